@@ -1,0 +1,45 @@
+// Shared host-side helpers for libpearl_b200: error reporting and launch checks.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/pearl_b200.h"
+
+namespace pearl {
+
+void set_error(const std::string& msg);
+
+#define PEARL_CUDA_TRY(expr)                                                              \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      ::pearl::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" +     \
+                         __FILE__ + ":" + std::to_string(__LINE__));                      \
+      return PEARL_ERR_CUDA;                                                              \
+    }                                                                                     \
+  } while (0)
+
+#define PEARL_ARG_CHECK(cond, msg)          \
+  do {                                      \
+    if (!(cond)) {                          \
+      ::pearl::set_error(std::string(msg)); \
+      return PEARL_ERR_ARG;                 \
+    }                                       \
+  } while (0)
+
+// Pairwise-sum plan for a vocabulary size (plan.cpp).
+struct VocabPlan {
+  int V = 0;
+  int C = 1;        // CTAs per row (thread-block cluster size)
+  int cap = 0;      // largest per-CTA slice length
+  int* d_plan = nullptr;  // C * kPlanStride ints on device
+};
+
+// Returns nullptr (and sets the error) if V was never prepared.
+const VocabPlan* get_plan(int V);
+int prepare_plan(int V);
+
+}  // namespace pearl

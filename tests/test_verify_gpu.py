@@ -1,0 +1,190 @@
+"""GPU parity of K1 (pearl_spec_verify) and the pick / law kernels.
+
+Bit-exact against the reference's golden outputs (tests/golden) on the same
+ProbDist rows and the same PCG64 uniforms, and against the oracle for the
+logits-mode device law.  Everything calls through the C ABI.
+"""
+
+import numpy as np
+import pytest
+
+import recipes
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def pk():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2408_11850_b200 as pk
+    return pk
+
+
+def _probs_rows(rows):
+    from oracle.probdist import normalize
+    return [torch.from_numpy(np.array(normalize(r)[0])).cuda() for r in rows]
+
+
+def _verify(pk, p_rows, q_rows, drafted, uniforms, flags=0, mode=0, inv_t=1.0, V=None):
+    from paper_2408_11850_b200 import _device, _lib
+    dev = torch.device("cuda")
+    V = V or int(p_rows[0].numel())
+    _lib.prepare_vocab(V)
+    sc = _device.scratch()
+    pr = _device.row_ptrs(p_rows, dev)
+    qr = _device.row_ptrs(q_rows, dev) if q_rows else None
+    toks = torch.tensor(drafted, dtype=torch.int32, device=dev)
+    u = torch.tensor(np.asarray(uniforms, dtype=np.float64), device=dev) if len(uniforms) else None
+    cursor = torch.zeros(1, dtype=torch.int32, device=dev)
+    acc = torch.zeros(len(drafted), dtype=torch.float64, device=dev)
+    code = _lib.load().pearl_spec_verify(
+        mode, _device.ptr(pr), _device.ptr(qr), _device.ptr(toks), len(drafted), V, _device.ptr(u),
+        0 if u is None else u.numel(), _device.ptr(cursor), inv_t, flags | _lib.F_ADVANCE,
+        _device.ptr(sc.result), _device.ptr(acc), _device.ptr(sc.verify_work), _device.stream_ptr())
+    _lib.check(code)
+    r = sc.result.cpu().numpy().tolist()
+    return dict(status=r[0], accepted=r[1], correction=r[2], examined=r[3], draws=r[4], bonus=r[5],
+                fallback=r[6], cursor=int(cursor.item()), accept=acc.cpu().numpy())
+
+
+def test_verify_cases_bit_exact(pk):
+    g = load_golden("verify_cases.json")
+    for case in g["cases"]:
+        ps, qs = recipes.make_rows(case["V"], case["n"], case["seed"], case["kind"])
+        P, Q = _probs_rows(ps), _probs_rows(qs)
+        rv = pk.RandomStream(case["seed"] + case["rng_seed"]).split(1)
+        us = rv.peek(case["n"] + 1)
+        assert list(us[:3]) == case["u_head"][: len(us[:3])]
+        r = _verify(pk, P, Q, case["drafted"], us)
+        got = (r["status"], r["accepted"], r["correction"], r["examined"], r["draws"], r["cursor"])
+        want = (0, case["accepted"], case["correction"], case["examined"], case["n_draws"], case["n_draws"])
+        assert got == want, (case["V"], case["kind"], case["n"], case["rng_seed"])
+        assert r["accept"].tolist() == case["accept_probs"]
+        rg = _verify(pk, P, None, case["drafted"], [], flags=1)
+        assert (rg["accepted"], rg["correction"], rg["draws"]) == (case["g_accepted"], case["g_correction"], 0)
+
+
+def test_verify_edge_cases(pk):
+    codes = {"AllZeroResidual": 2, "ZeroDraftProb": 3}
+    for case in load_golden("verify_cases.json")["edges"]:
+        P, Q = _probs_rows(case["p"]), _probs_rows(case["q"])
+        r = _verify(pk, P, Q, case["drafted"], case["uniforms"])
+        if case["error"]:
+            assert r["status"] == codes[case["error"]], case["name"]
+            assert r["draws"] == case["n_draws"], case["name"]
+        else:
+            assert (r["status"], r["accepted"], r["correction"], r["examined"], r["draws"]) == (
+                0, case["accepted"], case["correction"], case["examined"], case["n_draws"]), case["name"]
+
+
+def test_logits_mode_matches_reference_on_device_law(pk):
+    from oracle.probdist import logits_to_p1
+    from paper_2408_11850_b200 import _device, _lib
+    for case in load_golden("logits_cases.json"):
+        V, n = case["V"], case["n"]
+        lp = recipes.make_logits(V, n, case["seed"], kind=case["kind"])
+        lq = recipes.make_logits(V, n, case["seed"] + 1, kind=case["kind"])
+        tp = torch.from_numpy(lp).cuda()
+        tq = torch.from_numpy(lq).cuda()
+        # the device law itself is bit-identical to the oracle twin
+        _lib.prepare_vocab(V)
+        out = torch.empty((n, V), dtype=torch.float64, device="cuda")
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(_lib.load().pearl_logits_to_probs(_device.ptr(tp), n, V, case["inv_t"],
+                                                     _device.ptr(out), _device.ptr(st), _device.stream_ptr()))
+        assert int(st.item()) == 0
+        want = np.stack([logits_to_p1(r, case["inv_t"]) for r in lp])
+        assert np.array_equal(out.cpu().numpy(), want), (V, case["kind"])
+        rv = pk.RandomStream(case["seed"] * 3 + case["rng_seed"]).split(1)
+        r = _verify(pk, [tp[i] for i in range(n)], [tq[i] for i in range(n)], case["drafted"],
+                    rv.peek(n + 1), mode=1, inv_t=case["inv_t"], V=V)
+        assert (r["status"], r["accepted"], r["correction"], r["examined"], r["draws"]) == (
+            0, case["accepted"], case["correction"], case["examined"], case["n_draws"])
+        rg = _verify(pk, [tp[i] for i in range(n)], None, case["drafted"], [], flags=1, mode=1,
+                     inv_t=case["inv_t"], V=V)
+        assert (rg["accepted"], rg["correction"]) == (case["g_accepted"], case["g_correction"])
+
+
+def test_sample_cases_bit_exact(pk):
+    from paper_2408_11850_b200 import _device, _lib
+    for case in load_golden("sample_cases.json"):
+        ps, _ = recipes.make_rows(case["V"], 1, case["seed"], case["kind"])
+        row = _probs_rows(ps)[0]
+        V = case["V"]
+        _lib.prepare_vocab(V)
+        k = len(case["us"])
+        rows = _device.row_ptrs([row] * k, torch.device("cuda"))
+        u = torch.tensor(case["us"], dtype=torch.float64, device="cuda")
+        out = torch.empty(k, dtype=torch.int32, device="cuda")
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        work = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+        _lib.check(_lib.load().pearl_sample_rows(0, _device.ptr(rows), k, V, _device.ptr(u), k, None, 1.0, 0,
+                                                 _device.ptr(out), None, _device.ptr(st), _device.ptr(work),
+                                                 _device.stream_ptr()))
+        assert int(st.item()) == 0
+        assert out.cpu().tolist() == case["idx"], (V, case["kind"])
+
+
+def test_residual_and_api(pk):
+    from oracle.probdist import normalize
+    for case in load_golden("residual_cases.json"):
+        ps, qs = recipes.make_rows(case["V"], 1, case["seed"], case["kind"])
+        P, Q = pk.ProbDist(ps[0]), pk.ProbDist(qs[0])
+        r = pk.residual_dist(P, Q)
+        assert recipes.sha(r.probs) == case["sha_r"]
+        for u, want in zip(case["us"][:4], case["idx"][:4]):
+            class _R:
+                def peek(self, k):
+                    return np.array([u])
+
+                def consume(self, k):
+                    pass
+            assert pk.sample(r, _R()) == want
+    # API KATs (tests/test_sampling.py:11-77 of the reference)
+    p = pk.ProbDist([0.6, 0.4])
+    q = pk.ProbDist([0.4, 0.6])
+    assert pk.accept_prob(p, q, 0) == 1.0
+    assert pk.accept_prob(p, q, 1) == 0.4 / 0.6
+    with pytest.raises(pk.ZeroDraftProb):
+        pk.accept_prob(pk.ProbDist([0.5, 0.5, 0.0]), pk.ProbDist([0.5, 0.0, 0.5]), 1)
+    d = pk.ProbDist([0.3, 0.3, 0.4])
+    assert pk.verify_chain([0, 1, 2], [d] * 3, [d] * 3, pk.RandomStream(1)) == pk.VerifyResult(3, None, 3)
+    res = pk.verify_chain([1], [pk.one_hot(4, 1)], [pk.one_hot(4, 3)], pk.RandomStream(0))
+    assert (res.accepted_count, res.correction, res.examined) == (0, 3, 1)
+    d2 = pk.ProbDist([0.5, 0.5])
+    rng = pk.RandomStream(3)
+    pk.verify_chain([0, 1], [d2, d2], [d2, d2], rng)
+    assert rng.n_draws == 2
+    rng = pk.RandomStream(3)
+    pk.verify_chain([0, 0], [d2, pk.one_hot(2, 0)], [d2, pk.one_hot(2, 1)], rng)
+    assert rng.n_draws == 3
+    with pytest.raises(ValueError):
+        pk.verify_chain([0, 1], [d2], [d2, d2], pk.RandomStream(0))
+    assert pk.verify_chain([], [], [], pk.RandomStream(0)) == pk.VerifyResult(0, None, 0)
+    with pytest.raises(pk.AllZeroResidual):
+        pk.residual_dist(pk.ProbDist([0.25, 0.75]), pk.ProbDist([0.25, 0.75]))
+    np.testing.assert_allclose(pk.residual_dist(pk.ProbDist([0.4, 0.4, 0.2]), pk.ProbDist([0.1, 0.2, 0.7])).probs,
+                               [0.6, 0.4, 0.0], atol=1e-12)
+    assert all(pk.sample(pk.one_hot(6, 2), pk.RandomStream(0)) == 2 for _ in range(5))
+    _ = normalize
+
+
+def test_empirical_law_one_slot(pk):
+    """Single-slot output law == p (reference tests/test_sampling.py:80-115), 20k draws."""
+    from paper_2408_11850_b200 import _device, _lib
+    P, Q = [0.5, 0.3, 0.2], [0.2, 0.5, 0.3]
+    rng = np.random.default_rng(42)
+    N = 20000
+    counts = np.zeros(3)
+    p_row, q_row = _probs_rows([P, Q])
+    for _ in range(N // 2000):
+        us = rng.random((2000, 3))
+        for k in range(2000):
+            y = int(np.searchsorted(np.cumsum(Q), us[k, 0], side="right"))
+            r = _verify(pk, [p_row], [q_row], [y], us[k, 1:])
+            counts[y if r["accepted"] == 1 else r["correction"]] += 1
+    np.testing.assert_allclose(counts / N, P, atol=0.015)
