@@ -17,8 +17,11 @@ def run_smoke() -> None:
     # K1 on reference-style rows vs the oracle restatement
     rng = np.random.default_rng(0)
     V = 32000
-    ps = [normalize(rng.random(V) ** 8)[0] for _ in range(4)]
-    qs = [normalize(rng.random(V) ** 8)[0] for _ in range(4)]
+    def law():
+        x = rng.random(V) ** 8
+        return normalize(x / x.sum())[0]
+    ps = [law() for _ in range(4)]
+    qs = [law() for _ in range(4)]
     drafted = [int(np.argmax(q)) for q in qs]
     res = pk.verify_chain(drafted, [pk.ProbDist(q) for q in qs], [pk.ProbDist(p) for p in ps],
                           pk.RandomStream(7).split(1))
