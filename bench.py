@@ -1,0 +1,390 @@
+"""Benchmark: PEARL decoding on B200 (BASELINE.json metric, configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Workload (configs[1] of BASELINE.json): Llama-2-7B target + Llama-68M draft,
+random-init bf16 weights (controlled-alignment init, llama.py), batch 1,
+synthetic 128-token prompts, 128 new tokens, draft and target co-resident on
+one B200 (N=1).  A *step* is one ``decode_pearl`` call (prefill + decode of
+128 tokens) through the public API.  AR and fixed-gamma SD run on the same
+kernels in the same process for the speedup columns.
+
+Metric: generated tokens/s (whole job, all ranks), plus speedup vs AR and
+vs vanilla SD and mean accepted tokens per target forward.
+  value = tokens / device time of the decode graphs (inputs resident)
+  e2e   = tokens / wall time of the public API calls (host prompt in, host
+          tokens out: H2D of prompt + uniform tables, D2H of step summaries)
+Weights (13.6 GB) exceed L2 (126 MB), so every forward streams from HBM.
+
+N>1: one process per GPU (torchrun); each rank runs its own co-resident
+draft/target replica on its own prompt shard (replicas only, no data-path
+collective); value = all ranks' tokens / max-over-ranks time.
+
+--impl reference: the reference algorithm's CPU path (oracle/ port of
+pearl_lab's decode_pearl driving a PyTorch CPU Llama of the same
+architecture) timed on the host cores over a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "tokens/sec & speedup vs AR and vanilla SD; mean accepted tokens/target fwd"
+UNIT = "tokens/s"
+
+
+def _peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _traffic():
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) >= 9:
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _prompts(n, P, V, seed):
+    rng = np.random.default_rng(seed)
+    return [rng.integers(2, V, P).tolist() for _ in range(n)]
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    import paper_2408_11850_b200 as pk
+    from paper_2408_11850_b200 import _lib, llama
+
+    align = llama.AlignSpec(branch_std=args.branch_std, kappa=args.kappa)
+    target, draft = llama.build_pair(args.pair, gemm_target=args.gemm_target, align=align,
+                                     max_seq=args.prompt + args.new + 2 * args.gamma_max + 16, max_tokens=64,
+                                     temperature=1.0 if args.temperature <= 0 else args.temperature)
+    greedy = args.temperature <= 0
+    temp = 1.0 if greedy else args.temperature
+    V = target.cfg.vocab
+    prompts = _prompts(args.warmup + args.steps, args.prompt, V, seed=1000 + rank)
+
+    def cfg_for(gamma, seed, adaptive=False):
+        return pk.EngineConfig(gamma=gamma, max_new_tokens=args.new, seed=seed, greedy=greedy, temperature=temp,
+                               adaptive_gamma=adaptive, gamma_max=args.gamma_max)
+
+    pearl_gamma = args.gamma
+
+    def run(kind, i):
+        if kind == "pearl":
+            return pk.decode_pearl(draft, target, prompts[i], cfg_for(pearl_gamma, 17 + i, args.adaptive))
+        if kind == "sd":
+            return pk.decode_sd(draft, target, prompts[i], cfg_for(args.sd_gamma, 17 + i))
+        return pk.decode_autoregressive(target, prompts[i], cfg_for(1, 17 + i))
+
+    results = {}
+    clocks = None
+    for kind in ("ar", "sd", "pearl"):  # PEARL last: its clocks are sampled
+        for i in range(args.warmup):
+            run(kind, i)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        if kind == "pearl":
+            clocks = Clocks(local)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        ev0.record()
+        res = [run(kind, args.warmup + i) for i in range(args.steps)]
+        ev1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ev_s = ev0.elapsed_time(ev1) / 1e3
+        if kind == "pearl":
+            clocks = clocks.stop()
+        toks = sum(len(r.tokens) for r in res)
+        dev = sum(r.stats["device_s"] for r in res)
+        steps = [s for r in res for s in r.steps]
+        results[kind] = dict(tokens=toks, device_s=dev, wall_s=wall, event_s=ev_s,
+                             launches=sum(r.stats["launches"] for r in res),
+                             mean_tok_per_fwd=pk.mean_tokens_per_target_forward(steps),
+                             alpha=pk.empirical_acceptance(steps) if kind != "ar" else None,
+                             gamma=res[0].stats.get("gamma"),
+                             fallbacks=sum(r.stats.get("fallbacks", 0) for r in res))
+    # max over ranks of the timed region, sum of tokens
+    agg = {}
+    for kind, r in results.items():
+        vals = torch.tensor([r["device_s"], r["event_s"], r["wall_s"], float(r["tokens"])], device="cuda",
+                            dtype=torch.float64)
+        if ws > 1:
+            mx = vals.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = vals.clone()
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            agg[kind] = (mx[0].item(), mx[1].item(), mx[2].item(), sm[3].item())
+        else:
+            agg[kind] = tuple(vals.tolist())
+    # roofline of the dominant kernel sequence: one target window forward
+    rl = roofline(target, draft, pearl_gamma if not args.adaptive else results["pearl"]["gamma"], args)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(target, draft, prompts[0], args, greedy, temp)
+    if rank != 0:
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return None
+    dp, ep, wp, tp = agg["pearl"]
+    da, ea, wa, ta = agg["ar"]
+    ds_, es, wsd, ts_ = agg["sd"]
+    value = tp / dp
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1e3 * ep / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic prompts (uniform random ids), random-init weights (controlled-alignment init)",
+        "config": {
+            "workload": f"{args.pair} PEARL, batch 1, prompt {args.prompt}, {args.new} new tokens, "
+                        f"{'greedy T=0' if greedy else f'T={temp}'}, draft+target co-resident per GPU",
+            "pair": args.pair, "global_batch": ws, "prompt_len": args.prompt, "new_tokens": args.new,
+            "gamma": results["pearl"]["gamma"], "adaptive_gamma": bool(args.adaptive),
+            "sd_gamma": args.sd_gamma, "temperature": 0.0 if greedy else temp,
+            "target_gemm": args.gemm_target, "parallelism": f"replicas x{ws}",
+            "l2": "weights 13.6 GB >> 126 MB L2: every forward streams HBM (no flush needed)",
+        },
+        "e2e": {"value": round(tp / ep, 2), "unit": UNIT,
+                "h2d_bytes_per_step": 4 * (args.prompt + 1) + 8 * 2 * 4096,
+                "d2h_bytes_per_step": 4 * 32 * max(1, results["pearl"]["tokens"] // max(1, args.steps))},
+        "ar_tokens_per_s": round(ta / da, 2),
+        "sd_tokens_per_s": round(ts_ / ds_, 2),
+        "speedup_vs_ar": round((tp / dp) / (ta / da), 3),
+        "speedup_vs_sd": round((tp / dp) / (ts_ / ds_), 3),
+        "e2e_speedup_vs_ar": round((tp / ep) / (ta / ea), 3),
+        "mean_accepted_tokens_per_target_fwd": round(results["pearl"]["mean_tok_per_fwd"], 3),
+        "sd_mean_tokens_per_target_fwd": round(results["sd"]["mean_tok_per_fwd"], 3),
+        "alpha_hat": None if results["pearl"]["alpha"] is None else round(results["pearl"]["alpha"], 4),
+        "sd_alpha_hat": None if results["sd"]["alpha"] is None else round(results["sd"]["alpha"], 4),
+        "gpu_launches": int(results["pearl"]["launches"]),
+        "exact_cdf_fallbacks": int(results["pearl"]["fallbacks"]),
+        "roofline": rl,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def roofline(target, draft, gamma, args):
+    """Dominant kernel sequence = one target window forward (M = gamma tokens).
+
+    Algorithmic bytes per forward = bf16 weights + KV read over the context +
+    fp32 logits written; time = CUDA-event average of the forward on its
+    stream, after warm-up.
+    """
+    import torch
+    peak, src = _peaks()
+    M = max(1, int(gamma))
+    ctx = args.prompt + args.new // 2
+    toks = torch.full((M,), 5, dtype=torch.int32, device="cuda")
+    pos = torch.tensor([ctx], dtype=torch.int32, device="cuda")
+    out = torch.empty(M, target.cfg.vocab, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        target.forward(toks, M, pos, 0, out)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 10
+    s.record()
+    for _ in range(n):
+        target.forward(toks, M, pos, 0, out)
+    e.record()
+    e.synchronize()
+    t = s.elapsed_time(e) / 1e3 / n
+    c = target.cfg
+    byts = c.weight_bytes() + c.kv_bytes_per_token() * (ctx + M) + 4 * M * c.vocab
+    achieved = byts / t / 1e9
+    tr = _traffic().get(f"{c.name}_M{M}")
+    target.reset_adapter()
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": tr,
+            "kernel": f"target window forward ({c.name}, M={M}, ctx={ctx}, {args.gemm_target} GEMMs)",
+            "bytes_per_launch": int(byts), "ms_per_launch": round(t * 1e3, 4), "peak_source": src}
+
+
+def cpu_baseline(target, draft, prompt, args, greedy, temp):
+    """The reference algorithm's CPU path on the host cores, bounded sample."""
+    import torch
+    from oracle import engine as oe
+    from oracle.llama import OracleLlama
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    n_new = args.cpu_new
+    P = min(len(prompt), args.cpu_prompt)
+    mt = OracleLlama(target.cfg, _to_cpu(target.w), device="cpu", bf16_points=True, max_seq=P + n_new + 64,
+                     mm_dtype=torch.bfloat16, temperature=temp)
+    md = OracleLlama(draft.cfg, _to_cpu(draft.w), device="cpu", bf16_points=True, max_seq=P + n_new + 64,
+                     mm_dtype=torch.bfloat16, temperature=temp)
+    t0 = time.perf_counter()
+    toks, steps = oe.decode_pearl(md, mt, prompt[:P], args.gamma, n_new, seed=17, greedy=greedy)
+    dt = time.perf_counter() - t0
+    del mt, md
+    return {"value": round(len(toks) / dt, 4), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle decode_pearl (pearl_lab engines.py restated) + PyTorch CPU bf16 Llama, "
+                      f"{target.cfg.name}/{draft.cfg.name}, prompt {P}, {len(toks)} new tokens, gamma {args.gamma}",
+            "seconds": round(dt, 2)}
+
+
+def _to_cpu(w):
+    out = {k: v.cpu() for k, v in w.items() if k != "layers"}
+    out["layers"] = [{k: v.cpu() for k, v in L.items()} for L in w["layers"]]
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the CPU port alone (rank 0 only)."""
+    ws, rank, local = _dist()
+    if rank != 0:
+        return None
+    import torch
+    from oracle import engine as oe
+    from oracle.llama import OracleLlama
+    from paper_2408_11850_b200.llama import AlignSpec, PRESETS, PAIRS, init_weights, _shared_tables
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    tname, dname = PAIRS[args.pair]
+    tc, dc = PRESETS[tname], PRESETS[dname]
+    align = AlignSpec(branch_std=args.branch_std, kappa=args.kappa)
+    # weights are generated where it is fast (the GPU when present: same
+    # values as the GPU arm) and then moved to host memory; only the CPU
+    # decode below is timed.
+    gen_dev = "cuda" if torch.cuda.is_available() else "cpu"
+    shared = _shared_tables(tc.vocab, align, gen_dev)
+    tw = _to_cpu(init_weights(tc, align, align.seed + 1, gen_dev, shared))
+    dw = _to_cpu(init_weights(dc, align, align.seed + 2, gen_dev, shared))
+    del shared
+    greedy = args.temperature <= 0
+    temp = 1.0 if greedy else args.temperature
+    P = args.cpu_prompt
+    mt = OracleLlama(tc, tw, device="cpu", max_seq=P + args.cpu_new + 64, mm_dtype=torch.bfloat16, temperature=temp)
+    md = OracleLlama(dc, dw, device="cpu", max_seq=P + args.cpu_new + 64, mm_dtype=torch.bfloat16, temperature=temp)
+    prompts = _prompts(args.warmup + args.steps, P, tc.vocab, seed=1000)
+    for i in range(min(args.warmup, 1)):
+        oe.decode_pearl(md, mt, prompts[i], args.gamma, 2, seed=i, greedy=greedy)
+    t0 = time.perf_counter()
+    toks = 0
+    for i in range(args.steps):
+        out, _ = oe.decode_pearl(md, mt, prompts[args.warmup + i], args.gamma, args.cpu_new, seed=17 + i,
+                                 greedy=greedy)
+        toks += len(out)
+    dt = time.perf_counter() - t0
+    v = toks / dt
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic prompts, random-init weights",
+            "config": {"workload": f"{args.pair} PEARL on host CPU cores, bounded sample", "pair": args.pair,
+                       "prompt_len": P, "new_tokens": args.cpu_new, "gamma": args.gamma},
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} x decode_pearl of {args.cpu_new} tokens, prompt {P}"},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pair", default="llama2-7b/68m")
+    ap.add_argument("--gamma", type=int, default=4)
+    ap.add_argument("--sd-gamma", type=int, default=4)
+    ap.add_argument("--gamma-max", type=int, default=32)
+    ap.add_argument("--adaptive", action="store_true")
+    ap.add_argument("--prompt", type=int, default=128)
+    ap.add_argument("--new", type=int, default=128)
+    ap.add_argument("--temperature", type=float, default=1.0)
+    ap.add_argument("--branch-std", type=float, default=2e-4)
+    ap.add_argument("--kappa", type=float, default=13.0)
+    ap.add_argument("--gemm-target", default="cudacore")
+    ap.add_argument("--cpu-new", type=int, default=4)
+    ap.add_argument("--cpu-prompt", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

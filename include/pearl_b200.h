@@ -67,6 +67,9 @@ typedef struct {
 /* Library identity / errors */
 int pearl_version(void);
 const char* pearl_last_error(void);
+/* Number of kernel launches the library has issued (captured nodes count
+ * once per capture); used to report gpu_launches per timed step. */
+unsigned long long pearl_launch_count(void);
 
 /* Size in bytes of the scratch `work` buffer pearl_spec_verify needs for a
  * chain of n positions.  The buffer must be zero-initialised once; the
@@ -118,6 +121,105 @@ int pearl_logits_to_probs(const float* logits, int n_rows, int V, float inv_temp
  * the mass is below 1e-15. */
 int pearl_residual(const double* p, const double* q, int V, double* out, int32_t* status,
                    void* stream);
+
+
+/* ======================================================================== *
+ * Llama decoder runtime (replaces SequenceModel.next_dist, models.py:58-71,
+ * for GPU models: the draft's per-token forward inside _draft_block,
+ * engines.py:277-282, and the target's window forward,
+ * engines.py:302 / 373 / 425 / 492).
+ * ======================================================================== */
+
+/* Linear-layer engine of a model. */
+#define PEARL_GEMM_CUDACORE 0 /* batch-invariant 128-bit GEMV (draft, K2) */
+#define PEARL_GEMM_TCGEN05 1  /* tcgen05 + TMA small-M contraction (target, K3) */
+
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, vocab;
+  int32_t max_seq;    /* KV-cache capacity (positions)                  */
+  int32_t max_tokens; /* largest window processed in one pass (chunking) */
+  int32_t gemm_kind;  /* PEARL_GEMM_*                                    */
+  float norm_eps;
+  float reserved;
+} pearl_llama_config;
+
+/* Weight / cache pointer table, in this order (all device pointers):
+ *   0 embed      bf16 [V, d]          1 final_norm fp32 [d]
+ *   2 lm_head    bf16 [V, d]          3 rope_cos   fp32 [max_seq, hd/2]
+ *   4 rope_sin   fp32 [max_seq, hd/2] 5 k_cache    bf16 [L, max_seq, KV, hd]
+ *   6 v_cache    bf16 [L, max_seq, KV, hd]
+ *   then per layer l (base 7 + 6 l):
+ *     attn_norm fp32 [d], wqkv bf16 [(H+2KV) hd, d], wo bf16 [d, H hd],
+ *     mlp_norm fp32 [d], w_gate_up bf16 [2 ffn, d] (rows 2j = gate_j,
+ *     2j+1 = up_j), w_down bf16 [d, ffn]                                  */
+#define PEARL_LLAMA_FIXED_PTRS 7
+#define PEARL_LLAMA_PTRS_PER_LAYER 6
+
+int pearl_llama_create(const pearl_llama_config* cfg, const void* const* ptrs, int n_ptrs,
+                       void** handle);
+int pearl_llama_destroy(void* handle);
+
+/* Forward flags */
+#define PEARL_FWD_ADVANCE 1     /* *pos += n_tokens when done              */
+#define PEARL_FWD_LAST_LOGITS 2 /* logits only for the last token ([1, V]) */
+
+/* Run n_tokens tokens (device int32[n_tokens]) at positions *pos .. *pos+n-1
+ * (pos is a device int32 so graph replays see its current value), append
+ * their K/V to the cache and write fp32 logits [n_tokens, V] (or [1, V]).
+ * Per-token results are bitwise independent of n_tokens (batch invariance),
+ * which is what makes GPU PEARL / SD greedy output token-identical to AR. */
+int pearl_llama_forward(void* handle, const int32_t* tokens, int n_tokens, int32_t* pos,
+                        int flags, float* logits, void* stream);
+
+size_t pearl_llama_workspace_bytes(void* handle, int n_tokens);
+
+/* ======================================================================== *
+ * PEARL step bookkeeping on the device (engines.py:397-526 state updates)
+ * ======================================================================== */
+
+typedef struct {
+  int32_t committed_len; /* len(DecodeState.committed), prefix included  */
+  int32_t n_pending;     /* len(DecodeState.pending)                     */
+  int32_t mode;          /* 0 PRE_VERIFY, 1 POST_VERIFY                  */
+  int32_t target_pos;    /* target KV length (== committed_len - 1)      */
+  int32_t draft_pos;     /* draft KV length                              */
+  int32_t verify_cursor; /* uniforms used from the verify stream table   */
+  int32_t draft_cursor;  /* uniforms used from the draft stream table    */
+  int32_t last_status;
+} pearl_seq_state;
+
+/* K5 -- in-place KV rollback: cache length[i] = new_len[i] (no data moves;
+ * positions past the new length are overwritten by the next window). */
+int pearl_kv_rollback(int32_t* cache_len, const int32_t* new_len, int n, void* stream);
+
+typedef struct {
+  pearl_seq_state* state;
+  int32_t* seq_tokens;        /* committed tokens, capacity max_len       */
+  int32_t max_len;
+  const int32_t* chain;       /* k pending + fresh drafts xs[0..gamma)    */
+  int32_t k;                  /* pending count verified this step         */
+  int32_t gamma;              /* fresh drafts this step                   */
+  const pearl_verify_result* verdict;
+  int32_t* pending_tok;       /* [gamma_max] next pending ids             */
+  float* pending_rows;        /* [gamma_max, V] next pending q logits     */
+  const float* draft_rows;    /* [gamma, V] this step's draft logits      */
+  int32_t V;
+  int32_t sd_mode;            /* 1: draft-then-verify commit (bonus), no pending */
+  int32_t* out_host_view;     /* optional: [16 + gamma] summary for the host */
+} pearl_commit_args;
+
+/* Apply one verified step to the device-resident DecodeState: append the
+ * accepted chain plus correction (or SD bonus), roll both KV caches back to
+ * the accepted prefix, carry the unverified drafts (and their q rows) over
+ * as the next pending block, switch PRE/POST mode (engines.py:431-446,
+ * 500-515, 376-381). */
+int pearl_pearl_commit(const pearl_commit_args* args, void* stream);
+
+/* Build the next step's inputs from the device state: target window
+ * [committed[-1]] + pending, and the draft catch-up tokens
+ * committed+pending [draft_pos ..]. */
+int pearl_step_assemble(pearl_seq_state* state, const int32_t* seq_tokens, const int32_t* pending_tok,
+                        int32_t* target_in, int32_t* draft_in, int32_t* draft_in_count, void* stream);
 
 #ifdef __cplusplus
 }

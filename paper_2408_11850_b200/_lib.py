@@ -45,6 +45,7 @@ class VerifyResultC(ctypes.Structure):
 SIGNATURES = {
     "pearl_version": (_i32, []),
     "pearl_last_error": (ctypes.c_char_p, []),
+    "pearl_launch_count": (ctypes.c_ulonglong, []),
     "pearl_verify_work_bytes": (_sz, [_i32]),
     "pearl_prepare_vocab": (_i32, [_i32]),
     "pearl_spec_verify": (_i32, [_i32, _vp, _vp, _vp, _i32, _i32, _vp, _i32, _vp, _f32, _i32, _vp, _vp,
@@ -60,6 +61,7 @@ SIGNATURES = {
     "pearl_llama_workspace_bytes": (_sz, [_vp, _i32]),
     "pearl_kv_rollback": (_i32, [_vp, _vp, _i32, _vp]),
     "pearl_pearl_commit": (_i32, [_vp, _vp]),
+    "pearl_step_assemble": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lock = threading.Lock()

@@ -11,6 +11,9 @@
 namespace pearl {
 
 void set_error(const std::string& msg);
+// Every kernel launch issued by the library bumps this counter (read with
+// pearl_launch_count); during graph capture it counts captured nodes.
+void count_launch(int n = 1);
 
 #define PEARL_CUDA_TRY(expr)                                                              \
   do {                                                                                    \

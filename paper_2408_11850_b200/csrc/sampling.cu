@@ -553,6 +553,7 @@ int launch_clustered(K kernel, int n_clusters, int C, size_t smem, void* stream,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, args));
+  count_launch();
   return PEARL_OK;
 }
 

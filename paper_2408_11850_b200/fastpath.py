@@ -1,0 +1,461 @@
+r"""Device-resident decode loops for GPU models (the engines' fast path).
+
+One PEARL step (engines.py:397-526) is a single CUDA graph:
+
+    assemble  : target window [committed[-1]] + pending, draft catch-up ids
+    fork ---- draft stream : gamma x (draft forward M=1 -> inverse-CDF pick)    (K2 + pick)
+         \--- target stream: target forward over the window (M = k+1)         (K3/K4)
+    join (event rendezvous, the _PhaseRunner of engines.py:241-262)
+    K1        : fused verify of chain = pending + [x_0] (logits rows, fp64 law)
+    commit    : append accepted + correction, K5 KV rollback, carry pending,
+                flip PRE/POST (engines.py:431-446, 500-515)
+    D2H       : a 16+gamma int summary into pinned memory
+
+The host replays the graph for the current (k, gamma, m0) shape, waits for
+the summary and builds the StepTrace -- one sync per step.  SD
+(engines.py:344-394) and AR (engines.py:289-319) use the same kernels: SD as
+one serial graph per step, AR as graphs of 1/2/4/8 back-to-back steps.
+Uniforms come from the same split PCG64 streams as the reference, uploaded
+as tables and consumed through device cursors, so a seed gives the
+reference's tokens and traces.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import replace
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .core import RandomStream
+from .llama import LlamaModel, inv_temp
+
+_FWD_ADVANCE = 1
+_FWD_LAST = 2
+U_TABLE = 4096
+
+# pearl_seq_state field offsets (int32)
+S_COMMITTED, S_NPENDING, S_MODE, S_TPOS, S_DPOS, S_VCUR, S_DCUR, S_STATUS = range(8)
+# summary offsets (engine.cu SUM_*)
+SUM_STATUS, SUM_ACCEPTED, SUM_CORRECTION, SUM_EXAMINED, SUM_DRAWS, SUM_BONUS, SUM_COMMITTED, SUM_MODE, \
+    SUM_NPENDING, SUM_TPOS, SUM_DPOS, SUM_VCUR, SUM_DCUR, SUM_FALLBACK = range(14)
+SUM_HDR = 16
+
+
+class _VerifyResultC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("status", "accepted", "correction", "examined", "draws_used", "bonus", "fallback", "reserved")]
+
+
+class _CommitArgs(ctypes.Structure):
+    _fields_ = [("state", ctypes.c_void_p), ("seq_tokens", ctypes.c_void_p), ("max_len", ctypes.c_int32),
+                ("chain", ctypes.c_void_p), ("k", ctypes.c_int32), ("gamma", ctypes.c_int32),
+                ("verdict", ctypes.c_void_p), ("pending_tok", ctypes.c_void_p), ("pending_rows", ctypes.c_void_p),
+                ("draft_rows", ctypes.c_void_p), ("V", ctypes.c_int32), ("sd_mode", ctypes.c_int32),
+                ("out_host_view", ctypes.c_void_p)]
+
+
+def _addr(t: torch.Tensor, i: int = 0) -> int:
+    return int(t.data_ptr()) + i * t.element_size()
+
+
+class PairRuntime:
+    """Buffers and captured step graphs for one (draft, target) pair (or a target alone for AR)."""
+
+    def __init__(self, target: LlamaModel, draft: Optional[LlamaModel], gamma_max: int):
+        self.target, self.draft = target, draft
+        self.dev = target.device
+        V = target.cfg.vocab
+        if draft is not None and draft.cfg.vocab != V:
+            raise ValueError("draft and target must share a vocabulary")
+        self.V = V
+        self.gmax = int(gamma_max)
+        self.max_len = target.max_seq
+        if draft is not None:
+            self.max_len = min(self.max_len, draft.max_seq)
+        dev, g = self.dev, self.gmax
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.state = torch.zeros(8, **i32)
+        self.seq = torch.zeros(self.max_len + 2 * g + 4, **i32)
+        self.pending_tok = torch.zeros(g + 1, **i32)
+        self.pending_rows = torch.zeros(g + 1, V, dtype=torch.float32, device=dev)
+        self.draft_rows = torch.zeros(g + 1, V, dtype=torch.float32, device=dev)
+        self.target_rows = torch.zeros(g + 2, V, dtype=torch.float32, device=dev)
+        self.target_in = torch.zeros(g + 2, **i32)
+        self.chain = torch.zeros(2 * g + 2, **i32)
+        self.draft_in = torch.zeros(g + 4, **i32)
+        self.draft_cnt = torch.zeros(1, **i32)
+        self.verdict = torch.zeros(8, **i32)
+        self.summary = torch.zeros(SUM_HDR + g + 8, **i32)
+        self.summary_host = torch.zeros(SUM_HDR + g + 8, dtype=torch.int32).pin_memory()
+        self.u_draft = torch.zeros(U_TABLE, dtype=torch.float64, device=dev)
+        self.u_verify = torch.zeros(U_TABLE, dtype=torch.float64, device=dev)
+        wb = int(_lib.load().pearl_verify_work_bytes(g + 2))
+        self.work_v = torch.zeros(wb, dtype=torch.uint8, device=dev)
+        self.work_s = torch.zeros(wb, dtype=torch.uint8, device=dev)
+        self.sample_status = torch.zeros(1, **i32)
+        self.draft_row_ptrs = _device.row_ptrs([self.draft_rows[j] for j in range(g + 1)], dev)
+        self.target_row_ptrs = _device.row_ptrs([self.target_rows[j] for j in range(g + 2)], dev)
+        # q rows for a chain of k pending + 1 fresh: pending_rows[0..k-1], draft_rows[0]
+        self.q_row_ptrs = {k: _device.row_ptrs([self.pending_rows[j] for j in range(k)] + [self.draft_rows[0]], dev)
+                           for k in range(g + 1)}
+        # AR
+        self.ar_tok = torch.zeros(1, **i32)
+        self.ar_out = torch.zeros(8, **i32)
+        self.ar_out_host = torch.zeros(8, dtype=torch.int32).pin_memory()
+        self.graphs: Dict[tuple, torch.cuda.CUDAGraph] = {}
+        self.graph_launches: Dict[tuple, int] = {}
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        self.draft_stream = torch.cuda.Stream(device=dev, priority=-1)
+        self.target_stream = torch.cuda.Stream(device=dev)
+        self.lib = _lib.load()
+        _lib.prepare_vocab(V)
+
+    # -- kernel launch helpers (all graph-capturable) ---------------------
+    def _state_ptr(self, field: int) -> int:
+        return _addr(self.state, field)
+
+    def _pick(self, row_ptr_addr: int, out_addr: int, cursor_field: int, invt: float, greedy: bool,
+              table: torch.Tensor, stream, append: Optional[int] = None) -> None:
+        flags = (_lib.F_GREEDY if greedy else 0) | _lib.F_ADVANCE
+        _lib.check(self.lib.pearl_sample_rows(_lib.ROWS_LOGITS32, row_ptr_addr, 1, self.V, _device.ptr(table),
+                                              int(table.numel()), self._state_ptr(cursor_field), invt, flags,
+                                              out_addr, append, _device.ptr(self.sample_status),
+                                              _device.ptr(self.work_s), _device.stream_ptr(stream)), "pick")
+
+    def _draft_block(self, gamma: int, m0: int, xs_addr_fn, invt: float, greedy: bool, stream) -> None:
+        d = self.draft
+        pos = self._state_ptr(S_DPOS)
+        for j in range(gamma):
+            tok_addr = _device.ptr(self.draft_in) if j == 0 else xs_addr_fn(j - 1)
+            n = m0 if j == 0 else 1
+            _lib.check(self.lib.pearl_llama_forward(d.handle, tok_addr, n, pos, _FWD_ADVANCE | _FWD_LAST,
+                                                    _addr(self.draft_rows, j * self.V), _device.stream_ptr(stream)),
+                       "draft forward")
+            self._pick(_addr(self.draft_row_ptrs, j), xs_addr_fn(j), S_DCUR, invt, greedy, self.u_draft, stream)
+
+    def _verify(self, n: int, p_ptrs: torch.Tensor, q_ptrs: torch.Tensor, drafted_addr: int, invt: float,
+                greedy: bool, bonus: bool, stream) -> None:
+        flags = (_lib.F_GREEDY if greedy else 0) | _lib.F_ADVANCE | (_lib.F_BONUS if bonus else 0)
+        _lib.check(self.lib.pearl_spec_verify(_lib.ROWS_LOGITS32, _device.ptr(p_ptrs), _device.ptr(q_ptrs),
+                                              drafted_addr, n, self.V, _device.ptr(self.u_verify),
+                                              int(self.u_verify.numel()), self._state_ptr(S_VCUR), invt, flags,
+                                              _device.ptr(self.verdict), None, _device.ptr(self.work_v),
+                                              _device.stream_ptr(stream)), "spec_verify")
+
+    def _commit(self, chain_addr: int, k: int, gamma: int, sd: bool, stream) -> None:
+        a = _CommitArgs(self._state_ptr(0), _device.ptr(self.seq), self.max_len, chain_addr, k, gamma,
+                        _device.ptr(self.verdict), _device.ptr(self.pending_tok), _device.ptr(self.pending_rows),
+                        _device.ptr(self.draft_rows), self.V, 1 if sd else 0, _device.ptr(self.summary))
+        _lib.check(self.lib.pearl_pearl_commit(ctypes.byref(a), _device.stream_ptr(stream)), "commit")
+
+    def _assemble(self, stream) -> None:
+        _lib.check(self.lib.pearl_step_assemble(self._state_ptr(0), _device.ptr(self.seq),
+                                                _device.ptr(self.pending_tok), _device.ptr(self.target_in),
+                                                _device.ptr(self.draft_in), _device.ptr(self.draft_cnt),
+                                                _device.stream_ptr(stream)), "assemble")
+
+    # -- step bodies ----------------------------------------------------------
+    def _pearl_body(self, k: int, gamma: int, m0: int, invt: float, greedy: bool, concurrent: bool) -> None:
+        s0 = torch.cuda.current_stream()
+        self._assemble(s0)
+        xs_addr = lambda j: _addr(self.chain, k + j)  # noqa: E731
+        ptr_p = self.target_row_ptrs
+        ptr_q = self.q_row_ptrs[k]
+        tgt = self.target
+        if concurrent:
+            ds, ts = self.draft_stream, self.target_stream
+            ds.wait_stream(s0)
+            ts.wait_stream(s0)
+        else:
+            ds = ts = s0
+        with torch.cuda.stream(ds):
+            self._draft_block(gamma, m0, xs_addr, invt, greedy, ds)
+        with torch.cuda.stream(ts):
+            _lib.check(self.lib.pearl_llama_forward(tgt.handle, _device.ptr(self.target_in), k + 1,
+                                                    self._state_ptr(S_TPOS), 0, _device.ptr(self.target_rows),
+                                                    _device.stream_ptr(ts)), "target forward")
+        if concurrent:
+            s0.wait_stream(ds)
+            s0.wait_stream(ts)
+        # the chain's first k ids are the pending block: copy it in front of xs
+        if k > 0:
+            self.chain[:k].copy_(self.pending_tok[:k])
+        self._verify(k + 1, ptr_p, ptr_q, _device.ptr(self.chain), invt, greedy, False, s0)
+        self._commit(_device.ptr(self.chain), k, gamma, False, s0)
+        self.summary_host.copy_(self.summary, non_blocking=True)
+
+    def _sd_body(self, gamma: int, m0: int, invt: float, greedy: bool) -> None:
+        s0 = torch.cuda.current_stream()
+        self._assemble(s0)
+        chain = lambda j: _addr(self.target_in, 1 + j)  # noqa: E731  (xs live right after committed[-1])
+        self._draft_block(gamma, m0, chain, invt, greedy, s0)
+        _lib.check(self.lib.pearl_llama_forward(self.target.handle, _device.ptr(self.target_in), gamma + 1,
+                                                self._state_ptr(S_TPOS), 0, _device.ptr(self.target_rows),
+                                                _device.stream_ptr(s0)), "target forward")
+        q_ptrs = self.draft_row_ptrs
+        self._verify(gamma, self.target_row_ptrs, q_ptrs, chain(0), invt, greedy, True, s0)
+        self._commit(chain(0), 0, gamma, True, s0)
+        self.summary_host.copy_(self.summary, non_blocking=True)
+
+    def _ar_body(self, steps: int, invt: float, greedy: bool) -> None:
+        s0 = torch.cuda.current_stream()
+        for i in range(steps):
+            _lib.check(self.lib.pearl_llama_forward(self.target.handle, _device.ptr(self.ar_tok), 1,
+                                                    self._state_ptr(S_TPOS), _FWD_ADVANCE | _FWD_LAST,
+                                                    _device.ptr(self.target_rows), _device.stream_ptr(s0)),
+                       "target forward")
+            self._pick(_addr(self.target_row_ptrs, 0), _addr(self.ar_out, i), S_VCUR, invt, greedy, self.u_verify,
+                       s0, append=_device.ptr(self.ar_tok))
+        self.ar_out_host.copy_(self.ar_out, non_blocking=True)
+
+    def graph(self, key: tuple, body) -> torch.cuda.CUDAGraph:
+        g = self.graphs.get(key)
+        if g is None:
+            # warm up once eagerly on a side stream (cudaFuncSetAttribute etc.), then capture
+            g = torch.cuda.CUDAGraph()
+            c0 = int(self.lib.pearl_launch_count())
+            with torch.cuda.graph(g):
+                body()
+            self.graph_launches[key] = int(self.lib.pearl_launch_count()) - c0
+            self.graphs[key] = g
+        return g
+
+    def replay(self, key: tuple, body, stats: dict) -> None:
+        """Replay the step graph for ``key``, timing it on the device."""
+        g = self.graph(key, body)
+        self.ev[0].record()
+        g.replay()
+        self.ev[1].record()
+        self.ev[1].synchronize()
+        stats["device_s"] += self.ev[0].elapsed_time(self.ev[1]) / 1e3
+        stats["launches"] += self.graph_launches[key]
+        stats["replays"] += 1
+
+    # -- decode-level helpers ---------------------------------------------------
+    def reset(self, seq0: List[int], stats: Optional[dict] = None) -> None:
+        C = len(seq0)
+        c0 = int(self.lib.pearl_launch_count())
+        self.ev[2].record()
+        if C + 2 > self.max_len:
+            raise ValueError("prompt does not fit the KV cache")
+        self.seq[:C].copy_(torch.tensor(seq0, dtype=torch.int32))
+        st = torch.tensor([C, 0, 0, 0, 0, 0, 0, 0], dtype=torch.int32)
+        self.state.copy_(st)
+        # prefill both caches with all but the last committed token
+        if C > 1:
+            self.target.forward(self.seq[:C - 1], C - 1, self.state[S_TPOS:S_TPOS + 1], _FWD_ADVANCE, None)
+            if self.draft is not None:
+                self.draft.forward(self.seq[:C - 1], C - 1, self.state[S_DPOS:S_DPOS + 1], _FWD_ADVANCE, None)
+        self.ev[3].record()
+        self.ev[3].synchronize()
+        if stats is not None:
+            t = self.ev[2].elapsed_time(self.ev[3]) / 1e3
+            stats["device_s"] += t
+            stats["prefill_s"] += t
+            stats["launches"] += int(self.lib.pearl_launch_count()) - c0
+        self.target.reset_adapter()
+        if self.draft is not None:
+            self.draft.reset_adapter()
+
+    def load_uniforms(self, table: torch.Tensor, rng: RandomStream) -> None:
+        table.copy_(torch.from_numpy(np.array(rng.peek(U_TABLE))))
+
+
+class _Tables:
+    """Host mirror of a device uniform table + its stream."""
+
+    def __init__(self, rt: PairRuntime, table: torch.Tensor, rng: Optional[RandomStream], field: int):
+        self.rt, self.table, self.rng, self.field = rt, table, rng, field
+        self.host_cursor = 0
+        if rng is not None:
+            rt.load_uniforms(table, rng)
+
+    def advance(self, used_total_device: int, margin: int) -> None:
+        """Refill when the device cursor gets within ``margin`` of the end."""
+        self.host_cursor = used_total_device
+        if self.rng is not None and used_total_device > U_TABLE - margin:
+            self.rng.consume(used_total_device)
+            self.rt.load_uniforms(self.table, self.rng)
+            self.rt.state[self.field] = 0
+            self.host_cursor = 0
+
+
+def _runtime(target: LlamaModel, draft: Optional[LlamaModel], gamma_max: int) -> PairRuntime:
+    cache = target.__dict__.setdefault("_pearl_runtimes", {})
+    key = (id(draft), gamma_max)
+    rt = cache.get(key)
+    if rt is None:
+        rt = PairRuntime(target, draft, gamma_max)
+        cache[key] = rt
+    return rt
+
+
+def _new_stats(**kw) -> dict:
+    d = {"device_s": 0.0, "prefill_s": 0.0, "launches": 0, "replays": 0, "fallbacks": 0}
+    d.update(kw)
+    return d
+
+
+def _seq0(model: LlamaModel, prefix: Sequence[int]) -> List[int]:
+    return [model.bos_id] + [int(t) for t in prefix]
+
+
+def choose_gamma(cfg, target: LlamaModel, draft: LlamaModel) -> int:
+    """Adaptive draft length gamma = round(c), c = t_target / t_draft (paper §3.4;
+    theory.pearl_optimal_gamma), measured once per pair."""
+    if not cfg.adaptive_gamma:
+        return cfg.gamma
+    key = "_pearl_c_" + str(id(draft))
+    c = target.__dict__.get(key)
+    if c is None:
+        c = target.measure_forward_time(max(1, cfg.gamma)) / draft.measure_forward_time(1)
+        target.__dict__[key] = c
+    return int(max(1, min(cfg.gamma_max, round(c))))
+
+
+# -- engines ---------------------------------------------------------------
+
+
+def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], cfg, concurrent: bool = True):
+    from .engines import DecodeResult, StepTrace, finalize_step
+    gamma = choose_gamma(cfg, target, draft)
+    gmax = max(cfg.gamma_max, gamma, cfg.gamma)
+    t_d = gamma * draft.latency.forward_time  # (measured before the caches are filled)
+    t_t = target.latency.forward_time
+    rt = _runtime(target, draft, gmax)
+    seq0 = _seq0(target, prefix)
+    n0 = len(seq0)
+    stats = _new_stats(gamma=gamma)
+    rt.reset(seq0, stats)
+    root = RandomStream(cfg.seed)
+    tab_d = _Tables(rt, rt.u_draft, None if cfg.greedy else root.split(0), S_DCUR)
+    tab_v = _Tables(rt, rt.u_verify, None if cfg.greedy else root.split(1), S_VCUR)
+    invt = inv_temp(cfg.temperature)
+    committed: List[int] = list(seq0)
+    pending: List[int] = []
+    dpos = n0 - 1
+    steps: List = []
+    produced = 0
+    while produced < cfg.max_new_tokens:
+        if len(committed) + len(pending) + gamma + 2 >= rt.max_len:
+            raise ValueError("decode exceeds the KV-cache capacity (raise max_seq)")
+        k = len(pending)
+        m0 = len(committed) + k - dpos
+        key = ("pearl", k, gamma, m0, bool(cfg.greedy), invt, bool(concurrent))
+        rt.replay(key, lambda: rt._pearl_body(k, gamma, m0, invt, cfg.greedy, concurrent), stats)
+        s = rt.summary_host.numpy()
+        status = int(s[SUM_STATUS])
+        _lib.check(status, "decode_pearl step")
+        n_acc, corr = int(s[SUM_ACCEPTED]), int(s[SUM_CORRECTION])
+        xs = [int(t) for t in s[SUM_HDR:SUM_HDR + gamma]]
+        stats["fallbacks"] += int(s[SUM_FALLBACK])
+        chain = pending + [xs[0]]
+        kind = "pre_verify" if k == 0 and not steps_mode_post(steps) else "post_verify"
+        if corr < 0:
+            committed += chain
+            pending = xs[1:]
+            acc, cval, delta = k + 1, None, k + 1
+        else:
+            committed += chain[:n_acc] + [corr]
+            pending = []
+            acc, cval, delta = n_acc, corr, n_acc + 1
+        dpos = int(s[SUM_DPOS])
+        assert int(s[SUM_COMMITTED]) == len(committed)
+        if kind == "pre_verify":
+            acc = 1 if corr < 0 else 0
+        trace = StepTrace(len(steps), kind, tuple(xs), acc, cval, delta, t_d, t_t)
+        tab_v.advance(int(s[SUM_VCUR]), 2 * gmax + 8)
+        tab_d.advance(int(s[SUM_DCUR]), 2 * gmax + 8)
+        stop = finalize_step(tuple(committed), n0, produced, cfg)
+        if stop is not None:
+            steps.append(replace(trace, finalized_delta=stop - produced))
+            return DecodeResult(tuple(committed[n0:n0 + stop]), tuple(steps), stats=stats)
+        steps.append(trace)
+        produced = len(committed) - n0
+    return DecodeResult(tuple(committed[n0:]), tuple(steps), stats=stats)
+
+
+def steps_mode_post(steps) -> bool:
+    """Mode the engine is in before the next step: POST iff the last step fully accepted."""
+    return bool(steps) and steps[-1].correction is None
+
+
+def decode_sd(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], cfg):
+    from .engines import DecodeResult, StepTrace
+    gamma = cfg.gamma
+    t_d = gamma * draft.latency.forward_time
+    t_t = target.latency.forward_time
+    rt = _runtime(target, draft, max(cfg.gamma_max, gamma))
+    seq0 = _seq0(target, prefix)
+    n0 = len(seq0)
+    stats = _new_stats(gamma=gamma)
+    rt.reset(seq0, stats)
+    root = RandomStream(cfg.seed)
+    tab_d = _Tables(rt, rt.u_draft, None if cfg.greedy else root.split(0), S_DCUR)
+    tab_v = _Tables(rt, rt.u_verify, None if cfg.greedy else root.split(1), S_VCUR)
+    invt = inv_temp(cfg.temperature)
+    seq: List[int] = list(seq0)
+    dpos = n0 - 1
+    steps: List = []
+    done = False
+    while not done and len(seq) - n0 < cfg.max_new_tokens:
+        if len(seq) + gamma + 4 >= rt.max_len:
+            raise ValueError("decode exceeds the KV-cache capacity (raise max_seq)")
+        m0 = len(seq) - dpos
+        key = ("sd", gamma, m0, bool(cfg.greedy), invt)
+        rt.replay(key, lambda: rt._sd_body(gamma, m0, invt, cfg.greedy), stats)
+        s = rt.summary_host.numpy()
+        _lib.check(int(s[SUM_STATUS]), "decode_sd step")
+        n_acc, corr, bonus = int(s[SUM_ACCEPTED]), int(s[SUM_CORRECTION]), int(s[SUM_BONUS])
+        xs = [int(t) for t in s[SUM_HDR:SUM_HDR + gamma]]
+        block = xs[:n_acc] + [bonus if corr < 0 else corr]
+        appended = 0
+        for tok in block:
+            seq.append(tok)
+            appended += 1
+            if (cfg.eos_id is not None and tok == cfg.eos_id) or len(seq) - n0 >= cfg.max_new_tokens:
+                done = True
+                break
+        dpos = int(s[SUM_DPOS])
+        steps.append(StepTrace(len(steps), "sd", tuple(xs), min(n_acc, appended), None if corr < 0 else corr,
+                               appended, t_d, t_t))
+        tab_v.advance(int(s[SUM_VCUR]), 2 * gamma + 8)
+        tab_d.advance(int(s[SUM_DCUR]), 2 * gamma + 8)
+        stats["fallbacks"] += int(s[SUM_FALLBACK])
+    return DecodeResult(tuple(seq[n0:]), tuple(steps), stats=stats)
+
+
+def decode_autoregressive(target: LlamaModel, prefix: Sequence[int], cfg):
+    from .engines import DecodeResult, StepTrace
+    t_t = target.latency.forward_time
+    rt = _runtime(target, None, max(cfg.gamma_max, cfg.gamma))
+    seq0 = _seq0(target, prefix)
+    n0 = len(seq0)
+    stats = _new_stats()
+    rt.reset(seq0, stats)
+    rng = None if cfg.greedy else RandomStream(cfg.seed)
+    tab = _Tables(rt, rt.u_verify, rng, S_VCUR)
+    rt.ar_tok.fill_(seq0[-1])
+    invt = inv_temp(cfg.temperature)
+    out: List[int] = []
+    steps: List = []
+    while len(out) < cfg.max_new_tokens:
+        remaining = cfg.max_new_tokens - len(out)
+        G = 8 if remaining >= 8 else (4 if remaining >= 4 else (2 if remaining >= 2 else 1))
+        if n0 + len(out) + G + 1 >= rt.max_len:
+            raise ValueError("decode exceeds the KV-cache capacity (raise max_seq)")
+        if rng is not None and int(rt.state[S_VCUR].item()) + G > U_TABLE - 8:
+            tab.advance(int(rt.state[S_VCUR].item()), U_TABLE)
+        key = ("ar", G, bool(cfg.greedy), invt)
+        rt.replay(key, lambda: rt._ar_body(G, invt, cfg.greedy), stats)
+        toks = [int(t) for t in rt.ar_out_host.numpy()[:G]]
+        for tok in toks:
+            out.append(tok)
+            steps.append(StepTrace(len(steps), "ar", (), 0, None, 1, 0.0, t_t))
+            if cfg.eos_id is not None and tok == cfg.eos_id:
+                return DecodeResult(tuple(out), tuple(steps), stats=stats)
+    return DecodeResult(tuple(out), tuple(steps), stats=stats)

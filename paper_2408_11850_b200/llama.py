@@ -1,0 +1,341 @@
+"""GPU Llama SequenceModels: random-init weights of the named architectures.
+
+``LlamaModel`` is a ``SequenceModel`` (its ``next_dist`` is an adapter over
+the device forward, for the plugin path and for parity runs of the
+reference engine) and a *device model*: the engines' fast path drives its
+KV-cached forward (libpearl_b200 ``pearl_llama_forward``) directly.
+
+Architectures (public model-card values; PAPER.md:571-580 gives L/d/FFN,
+heads / KV heads / vocab are external):
+
+    llama2-7b    L32 d4096 H32/32 FFN11008 V32000      (target, C2)
+    llama-68m    L2  d768  H12/12 FFN3072  V32000      (draft,  C2)
+    dsc-33b      L62 d7168 H56/8  FFN19200 V32256      (target, C3)
+    dsc-1.3b     L24 d2048 H16/16 FFN5504  V32256      (draft,  C3)
+    llama3-70b   L80 d8192 H64/8  FFN28672 V128256     (target, C4)
+    llama3-8b    L32 d4096 H32/8  FFN14336 V128256     (draft,  C4)
+    tiny-target  L4  d512  H8/8   FFN1376  V32000      (C1, builder-defined)
+    tiny-draft   L2  d256  H4/4   FFN688   V32000      (C1)
+
+Controlled-alignment random init (no checkpoints exist offline; random
+independent pairs would accept ~0 drafts at T=0): both models of a pair share
+a rank-r bigram structure -- embeddings E = sqrt(d) * U_hat P and lm_head =
+kappa * U'_hat P / sqrt(d), with P an orthonormal r x d projection drawn per
+model, U_hat a shared random unit-row table and U' = U_hat permuted (token
+x's successor pi(x) scores kappa).  Every other weight is i.i.d. Gaussian
+(std 0.02; attention-out and MLP-down use ``branch_std``), so each model's
+context-dependent residual branches perturb the shared bigram law
+independently; ``branch_std`` is the alignment knob and the measured
+acceptance is always reported next to any speedup.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, replace
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .core import ProbDist
+from .models import LatencyProfile, SequenceModel
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    name: str
+    n_layers: int
+    d_model: int
+    n_heads: int
+    n_kv_heads: int
+    ffn: int
+    vocab: int
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-5
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_heads
+
+    def param_count(self) -> int:
+        d, hd = self.d_model, self.head_dim
+        per_layer = d * (self.n_heads + 2 * self.n_kv_heads) * hd + self.n_heads * hd * d + 3 * d * self.ffn + 2 * d
+        return self.n_layers * per_layer + 2 * self.vocab * d + d
+
+    def weight_bytes(self) -> int:
+        """bf16 bytes streamed per forward (norms are fp32 here but tiny)."""
+        d, hd = self.d_model, self.head_dim
+        mats = self.n_layers * (d * (self.n_heads + 2 * self.n_kv_heads) * hd + self.n_heads * hd * d
+                                + 3 * d * self.ffn) + self.vocab * d
+        return 2 * mats
+
+    def kv_bytes_per_token(self) -> int:
+        return 2 * self.n_layers * self.n_kv_heads * self.head_dim * 2
+
+
+PRESETS: Dict[str, LlamaConfig] = {
+    "llama2-7b": LlamaConfig("llama2-7b", 32, 4096, 32, 32, 11008, 32000),
+    "llama-68m": LlamaConfig("llama-68m", 2, 768, 12, 12, 3072, 32000),
+    "dsc-33b": LlamaConfig("dsc-33b", 62, 7168, 56, 8, 19200, 32256, rope_theta=100000.0, norm_eps=1e-6),
+    "dsc-1.3b": LlamaConfig("dsc-1.3b", 24, 2048, 16, 16, 5504, 32256, rope_theta=100000.0, norm_eps=1e-6),
+    "llama3-70b": LlamaConfig("llama3-70b", 80, 8192, 64, 8, 28672, 128256, rope_theta=500000.0),
+    "llama3-8b": LlamaConfig("llama3-8b", 32, 4096, 32, 8, 14336, 128256, rope_theta=500000.0),
+    "tiny-target": LlamaConfig("tiny-target", 4, 512, 8, 8, 1376, 32000),
+    "tiny-draft": LlamaConfig("tiny-draft", 2, 256, 4, 4, 688, 32000),
+}
+
+PAIRS = {
+    "tiny": ("tiny-target", "tiny-draft"),
+    "llama2-7b/68m": ("llama2-7b", "llama-68m"),
+    "dsc-33b/1.3b": ("dsc-33b", "dsc-1.3b"),
+    "llama3-70b/8b": ("llama3-70b", "llama3-8b"),
+}
+
+
+@dataclass(frozen=True)
+class AlignSpec:
+    """Controlled-alignment knobs of a random-init pair (see module doc)."""
+
+    rank: int = 64
+    kappa: float = 13.0
+    branch_std: float = 2e-4
+    seed: int = 1234
+
+
+def rope_tables(hd: int, max_seq: int, theta: float):
+    inv = theta ** (-np.arange(0, hd, 2, dtype=np.float64) / hd)
+    ang = np.arange(max_seq, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+def _shared_tables(V: int, align: AlignSpec, device) -> tuple:
+    g = torch.Generator(device=device)
+    g.manual_seed(align.seed)
+    U = torch.randn(V, align.rank, generator=g, device=device, dtype=torch.float32)
+    U = U / U.norm(dim=1, keepdim=True)
+    perm = torch.randperm(V, generator=g, device=device)
+    Uo = torch.empty_like(U)
+    Uo[perm] = U  # successor of token x is perm[x]: its output vector is U[x]
+    Uo = Uo + 0.05 * torch.randn(V, align.rank, generator=g, device=device) / math.sqrt(align.rank)
+    return U, Uo
+
+
+def init_weights(cfg: LlamaConfig, align: AlignSpec, model_seed: int, device,
+                 shared=None) -> Dict[str, object]:
+    """Random-init weights (bf16 matrices, fp32 norms) with the shared bigram structure."""
+    g = torch.Generator(device=device)
+    g.manual_seed(model_seed)
+    d, hd, H, KV, F, V = cfg.d_model, cfg.head_dim, cfg.n_heads, cfg.n_kv_heads, cfg.ffn, cfg.vocab
+    U, Uo = shared if shared is not None else _shared_tables(V, align, device)
+    q, _ = torch.linalg.qr(torch.randn(d, align.rank, generator=g, device=device, dtype=torch.float32))
+    P = q.T.contiguous()  # r x d, orthonormal rows
+    w: Dict[str, object] = {}
+    emb = torch.empty(V, d, dtype=torch.bfloat16, device=device)
+    head = torch.empty(V, d, dtype=torch.bfloat16, device=device)
+    for s in range(0, V, 16384):
+        emb[s:s + 16384] = (math.sqrt(d) * (U[s:s + 16384] @ P)).to(torch.bfloat16)
+        head[s:s + 16384] = (align.kappa / math.sqrt(d) * (Uo[s:s + 16384] @ P)).to(torch.bfloat16)
+    w["embed"], w["lm_head"] = emb, head
+    w["final_norm"] = torch.ones(d, dtype=torch.float32, device=device)
+
+    def rnd(rows, cols, std):
+        t = torch.empty(rows, cols, dtype=torch.bfloat16, device=device)
+        for s in range(0, rows, 4096):
+            e = min(rows, s + 4096)
+            t[s:e] = (torch.randn(e - s, cols, generator=g, device=device) * std).to(torch.bfloat16)
+        return t
+
+    layers = []
+    for _ in range(cfg.n_layers):
+        layers.append({
+            "attn_norm": torch.ones(d, dtype=torch.float32, device=device),
+            "wqkv": rnd((H + 2 * KV) * hd, d, 0.02),
+            "wo": rnd(d, H * hd, align.branch_std),
+            "mlp_norm": torch.ones(d, dtype=torch.float32, device=device),
+            "w_gate_up": rnd(2 * F, d, 0.02),  # rows 2j = gate_j, 2j+1 = up_j
+            "w_down": rnd(d, F, align.branch_std),
+        })
+    w["layers"] = layers
+    return w
+
+
+def init_pair(pair: str, align: AlignSpec = AlignSpec(), device=None):
+    """(target_weights, draft_weights, target_cfg, draft_cfg) for a named pair."""
+    device = device or _device.require_cuda()
+    tname, dname = PAIRS[pair]
+    tc, dc = PRESETS[tname], PRESETS[dname]
+    assert tc.vocab == dc.vocab
+    shared = _shared_tables(tc.vocab, align, device)
+    tw = init_weights(tc, align, align.seed + 1, device, shared)
+    dw = init_weights(dc, align, align.seed + 2, device, shared)
+    del shared
+    return tw, dw, tc, dc
+
+
+class _CConfig(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "ffn",
+                                              "vocab", "max_seq", "max_tokens", "gemm_kind")] + [
+        ("norm_eps", ctypes.c_float), ("reserved", ctypes.c_float)]
+
+
+GEMM_KINDS = {"cudacore": 0, "tcgen05": 1}
+
+
+class LlamaModel(SequenceModel):
+    """A random-init Llama on the GPU: SequenceModel + device fast-path model."""
+
+    _pearl_device_model = True
+
+    def __init__(self, cfg: LlamaConfig, weights: Dict[str, object], gemm: str = "cudacore",
+                 max_seq: int = 1024, max_tokens: int = 64, temperature: float = 1.0, bos_id: int = 1,
+                 latency: Optional[LatencyProfile] = None):
+        self.device = _device.require_cuda()
+        self.cfg = cfg
+        self.vocab_size = cfg.vocab
+        self.temperature = float(temperature)
+        self.bos_id = int(bos_id)
+        self.max_seq = int(max_seq)
+        self.max_tokens = int(max_tokens)
+        self.gemm = gemm
+        self.w = weights
+        hd = cfg.head_dim
+        cos, sin = rope_tables(hd, max_seq, cfg.rope_theta)
+        self.rope_cos = torch.from_numpy(cos).to(self.device)
+        self.rope_sin = torch.from_numpy(sin).to(self.device)
+        kv_shape = (cfg.n_layers, max_seq, cfg.n_kv_heads, hd)
+        self.k_cache = torch.zeros(kv_shape, dtype=torch.bfloat16, device=self.device)
+        self.v_cache = torch.zeros(kv_shape, dtype=torch.bfloat16, device=self.device)
+        ptrs = [weights["embed"], weights["final_norm"], weights["lm_head"], self.rope_cos, self.rope_sin,
+                self.k_cache, self.v_cache]
+        for L in weights["layers"]:
+            ptrs += [L["attn_norm"], L["wqkv"], L["wo"], L["mlp_norm"], L["w_gate_up"], L["w_down"]]
+        for t in ptrs:
+            assert t.is_cuda and t.is_contiguous()
+        self._ptr_arr = (ctypes.c_void_p * len(ptrs))(*[t.data_ptr() for t in ptrs])
+        c = _CConfig(cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.n_kv_heads, hd, cfg.ffn, cfg.vocab, max_seq,
+                     max_tokens, GEMM_KINDS[gemm], cfg.norm_eps, 0.0)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().pearl_llama_create(ctypes.byref(c), self._ptr_arr, len(ptrs), ctypes.byref(h)),
+                   "pearl_llama_create")
+        self.handle = h
+        _lib.prepare_vocab(cfg.vocab)
+        # adapter state (next_dist): tokens whose K/V occupy cache positions 0..n-1
+        self._pos = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._cached: List[int] = []
+        self._latency = latency
+
+    # -- device API -------------------------------------------------------
+    def forward(self, tokens: torch.Tensor, n: int, pos: torch.Tensor, flags: int, logits: Optional[torch.Tensor],
+                stream=None) -> None:
+        _lib.check(_lib.load().pearl_llama_forward(self.handle, _device.ptr(tokens), int(n), _device.ptr(pos),
+                                                   int(flags), _device.ptr(logits), _device.stream_ptr(stream)),
+                   "pearl_llama_forward")
+
+    def forward_logits(self, tokens: Sequence[int], start: int = 0) -> torch.Tensor:
+        """fp32 logits of every token of ``tokens`` placed at positions start.. (fresh cache)."""
+        toks = torch.tensor(list(tokens), dtype=torch.int32, device=self.device)
+        pos = torch.tensor([start], dtype=torch.int32, device=self.device)
+        out = torch.empty(len(tokens), self.cfg.vocab, dtype=torch.float32, device=self.device)
+        T = self.max_tokens
+        for s in range(0, len(tokens), T):
+            n = min(T, len(tokens) - s)
+            self.forward(toks[s:s + n], n, pos, 1, out[s:s + n])
+        self._cached = []  # cache content no longer tracks the adapter
+        return out
+
+    @property
+    def latency(self) -> LatencyProfile:
+        if self._latency is None:
+            self._latency = LatencyProfile(self.measure_forward_time(1))
+        return self._latency
+
+    @latency.setter
+    def latency(self, v: LatencyProfile) -> None:
+        self._latency = v
+
+    def measure_forward_time(self, n_tokens: int = 1, iters: int = 5) -> float:
+        """Measured seconds per forward of an n-token window (CUDA events)."""
+        toks = torch.full((n_tokens,), self.bos_id, dtype=torch.int32, device=self.device)
+        pos = torch.zeros(1, dtype=torch.int32, device=self.device)
+        out = torch.empty(n_tokens, self.cfg.vocab, dtype=torch.float32, device=self.device)
+        for _ in range(2):
+            self.forward(toks, n_tokens, pos, 0, out)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            self.forward(toks, n_tokens, pos, 0, out)
+        e.record()
+        e.synchronize()
+        self._cached = []
+        return s.elapsed_time(e) / 1e3 / iters
+
+    # -- SequenceModel adapter ---------------------------------------------
+    def next_dist(self, prefix: Sequence[int]) -> ProbDist:
+        """ProbDist of the device law after ``prefix`` (LCP-reused KV cache).
+
+        The law is the device softmax p1 of the fp32 logits (the same one the
+        fast path's kernels use), handed to ProbDist which renormalises it
+        exactly like the reference.
+        """
+        seq = [self.bos_id] + [int(t) for t in prefix]
+        lcp = 0
+        lim = min(len(self._cached), len(seq) - 1)
+        while lcp < lim and self._cached[lcp] == seq[lcp]:
+            lcp += 1
+        todo = seq[lcp:]
+        if len(seq) > self.max_seq:
+            raise ValueError("prefix exceeds the KV-cache capacity")
+        self._pos.fill_(lcp)
+        toks = torch.tensor(todo, dtype=torch.int32, device=self.device)
+        logits = torch.empty(1, self.cfg.vocab, dtype=torch.float32, device=self.device)
+        self.forward(toks, len(todo), self._pos, _FWD_LAST, logits)
+        self._cached = seq
+        return ProbDist(self.probs_from_logits(logits)[0].cpu().numpy())
+
+    def probs_from_logits(self, logits: torch.Tensor, temperature: Optional[float] = None) -> torch.Tensor:
+        t = self.temperature if temperature is None else temperature
+        n = logits.shape[0]
+        out = torch.empty(n, self.cfg.vocab, dtype=torch.float64, device=self.device)
+        st = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _lib.check(_lib.load().pearl_logits_to_probs(_device.ptr(logits), n, self.cfg.vocab,
+                                                     float(np.float32(1.0 / t)), _device.ptr(out),
+                                                     _device.ptr(st), _device.stream_ptr()), "logits_to_probs")
+        _lib.check(int(st.item()), "logits_to_probs")
+        return out
+
+    def reset_adapter(self) -> None:
+        self._cached = []
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.load().pearl_llama_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_FWD_ADVANCE = 1
+_FWD_LAST = 2
+
+
+def inv_temp(t: float) -> float:
+    """fp32 inverse temperature exactly as the kernels receive it."""
+    return float(np.float32(1.0 / t))
+
+
+def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: str = "cudacore",
+               align: AlignSpec = AlignSpec(), max_seq: int = 1024, max_tokens: int = 64,
+               temperature: float = 1.0):
+    """(target LlamaModel, draft LlamaModel) with controlled-alignment random weights."""
+    tw, dw, tc, dc = init_pair(pair, align)
+    target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature)
+    draft = LlamaModel(dc, dw, gemm=gemm_draft, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature)
+    return target, draft
