@@ -173,6 +173,13 @@ int pearl_llama_forward(void* handle, const int32_t* tokens, int n_tokens, int32
 
 size_t pearl_llama_workspace_bytes(void* handle, int n_tokens);
 
+/* Standalone contraction Y[M, N] (fp32) = X[M, K] (bf16) . W[N, K]^T (bf16)
+ * on the given engine (PEARL_GEMM_*), for tests and microbenchmarks.
+ * splits = 0 lets the planner pick the split-K factor (tcgen05 only). */
+int pearl_gemm(int kind, const void* W, const void* X, float* Y, int M, int N, int K, int splits, void* stream);
+/* Split-K factor the tcgen05 planner uses for an (N, K) weight. */
+int pearl_gemm_splits(int N, int K);
+
 /* ======================================================================== *
  * PEARL step bookkeeping on the device (engines.py:397-526 state updates)
  * ======================================================================== */

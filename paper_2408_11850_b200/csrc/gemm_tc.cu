@@ -1,16 +1,387 @@
-// K3 placeholder: tcgen05 path not yet wired (returns an argument error).
+// K3: tcgen05 + TMA small-M contraction (see gemm_tc.cuh).
+//
+// CTA = 4 warps, one (row tile, K split) unit:
+//   warp 0 / lane 0 : TMA producer -- 128x64 W tile + NT 16x64 X tiles per
+//                     stage into a kStages-deep smem ring (SWIZZLE_128B)
+//   warp 1          : TMEM allocator; lane 0 issues tcgen05.mma
+//                     (M=128, N=16, K=16, bf16 -> fp32) and tcgen05.commit
+//                     releases each smem stage back to the producer
+//   all 4 warps     : epilogue -- tcgen05.ld 32x32b (warp w owns TMEM lanes
+//                     32w..32w+31 = weight rows), fixed-order split-K sum by
+//                     the last-arriving CTA, then the shared fused epilogue.
 #include "gemm_tc.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+
+#include "epilogue.cuh"
+
 namespace pearl {
-int tc_init(TcGemmCtx& ctx, const pearl_llama_config& cfg) {
-  (void)ctx;
-  (void)cfg;
-  set_error("tcgen05 GEMM path not built yet");
-  return PEARL_ERR_ARG;
+
+constexpr int kTcStages = 6;
+constexpr int kTileN = 128;    // weight rows per tile (MMA-M)
+constexpr int kTileK = 64;     // K per stage (one 128-byte swizzle row)
+constexpr int kTokTile = 16;   // tokens per MMA (MMA-N)
+constexpr int kMaxTokTiles = 4;
+constexpr int kWBytes = kTileN * kTileK * 2;        // 16 KB
+constexpr int kXBytes = kTokTile * kTileK * 2;      // 2 KB per token tile
+constexpr int kStageBytes = kWBytes + kMaxTokTiles * kXBytes;  // 24 KB
+constexpr int kTcThreads = 128;
+constexpr size_t kTcSmem = 1024 /*align slack*/ + static_cast<size_t>(kTcStages) * kStageBytes + 256;
+
+struct TcArgs {
+  int M, N, K, KB, S;
+  EpiArgs e;
+  float* partials;
+  int* flags;
+};
+
+// ---- PTX helpers -----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-void tc_free(TcGemmCtx& ctx) { (void)ctx; }
-int tc_gemm(TcGemmCtx&, const __nv_bfloat16*, const __nv_bfloat16*, int, int, int, const EpiArgs&, cudaStream_t) {
-  set_error("tcgen05 GEMM path not built yet");
-  return PEARL_ERR_ARG;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem_tile) {
+  // K-major SWIZZLE_128B canonical layout: rows of 128 B, 8-row groups 1024 B
+  // apart (SBO = 1024 B), LBO = 16 B (unused for swizzled K-major), version 1.
+  const uint64_t addr = smem_u32(smem_tile);
+  return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// instruction descriptor: D=f32, A=B=bf16, K-major both, N=16, M=128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((kTokTile >> 3) << 17) | ((kTileN >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---- kernel ------------------------------------------------------------------
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+  // 1024-byte alignment for SWIZZLE_128B
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * kStageBytes);
+  uint64_t* empty = full + kTcStages;
+  uint64_t* accum = empty + kTcStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x / a.S;
+  const int split = blockIdx.x % a.S;
+  const int kb0 = static_cast<int>((static_cast<long long>(split) * a.KB) / a.S);
+  const int kb1 = static_cast<int>((static_cast<long long>(split + 1) * a.KB) / a.S);
+  const int nkb = kb1 - kb0;
+  const int NT = (a.M + kTokTile - 1) / kTokTile;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+  }
+  if (warp == 1) {
+    // 64 fp32 columns: up to 4 token tiles of 16
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    const uint32_t bytes = kWBytes + NT * kXBytes;
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kTcStages;
+      if (i >= kTcStages) mbar_wait(&empty[s], ((i / kTcStages) - 1) & 1);
+      unsigned char* st = smem + s * kStageBytes;
+      mbar_expect_tx(&full[s], bytes);
+      const int kc = (kb0 + i) * kTileK;
+      tma_load_2d(st, &tmW, &full[s], kc, tile * kTileN);
+      for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kTcStages;
+      mbar_wait(&full[s], (i / kTcStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      unsigned char* st = smem + s * kStageBytes;
+      const uint64_t adesc = umma_desc_sw128(st);
+      for (int j = 0; j < NT; ++j) {
+        const uint64_t bdesc = umma_desc_sw128(st + kWBytes + j * kXBytes);
+#pragma unroll
+        for (int kk = 0; kk < kTileK / 16; ++kk) {
+          // advance 16 bf16 = 32 bytes along K inside the swizzle row
+          umma_bf16(tmem + j * kTokTile, adesc + 2 * kk, bdesc + 2 * kk, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(accum);
+  }
+  __syncwarp();
+  // ---- epilogue (all warps)
+  mbar_wait(accum, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  float* E = reinterpret_cast<float*>(smem);  // [128][64] fp32 staging, reuses the ring
+  const int row = warp * 32 + lane;
+  const int TOKP = NT * kTokTile;
+  float v[16];
+  for (int j = 0; j < NT; ++j) {
+    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + j * kTokTile, v);
+    if (a.S == 1) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) E[row * 64 + j * 16 + c] = v[c];
+    } else {
+      float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * TOKP + j * kTokTile;
+#pragma unroll
+      for (int c = 0; c < 16; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (a.S > 1) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(&a.flags[tile], 1) == a.S - 1);
+    __syncthreads();
+    if (!s_last) {
+      if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+      return;
+    }
+    __threadfence();
+    // fixed split order => result independent of arrival order and of M
+    for (int t = 0; t < a.M; ++t) {
+      float acc = 0.f;
+      for (int s = 0; s < a.S; ++s)
+        acc += __ldcg(a.partials + ((static_cast<size_t>(tile) * a.S + s) * kTileN + row) * TOKP + t);
+      E[row * 64 + t] = acc;
+    }
+    if (threadIdx.x == 0) a.flags[tile] = 0;
+  }
+  __syncthreads();
+  // fused epilogue over (4-row group, token)
+  const int groups = kTileN / 4;
+  for (int idx = threadIdx.x; idx < groups * a.M; idx += blockDim.x) {
+    const int g = idx % groups, t = idx / groups;
+    const int n0 = tile * kTileN + g * 4;
+    if (n0 >= a.N) continue;
+    float w[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) w[r] = E[(g * 4 + r) * 64 + t];
+    epilogue4(a.e, t, n0, w, a.N);
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+}
+
+// ---- host side ---------------------------------------------------------------
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_enc_once;
+
+int get_encoder() {
+  std::call_once(g_enc_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return PEARL_ERR_CUDA;
+  }
+  return PEARL_OK;
+}
+
+int encode_2d(CUtensorMap* map, const void* base, int inner, int rows, int box_rows) {
+  int rc = get_encoder();
+  if (rc) return rc;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kTileK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+    return PEARL_ERR_CUDA;
+  }
+  return PEARL_OK;
+}
+
+std::once_flag g_attr_once;
+cudaError_t g_attr_err = cudaSuccess;
+
+}  // namespace
+
+int tc_splits(int N, int K, int num_sms) {
+  const int tiles = (N + kTileN - 1) / kTileN;
+  const int KB = (K + kTileK - 1) / kTileK;
+  int best = 1;
+  long long best_cost = -1;
+  for (int S = 1; S <= std::min(KB, 32); ++S) {
+    if (KB / S < 4 && S > 1) break;  // keep >= 4 k-blocks of streaming per CTA
+    const long long ctas = static_cast<long long>(tiles) * S;
+    const long long waves = (ctas + num_sms - 1) / num_sms;
+    const long long per = (KB + S - 1) / S;
+    // per-SM streamed k-blocks + a small cost per partial tile written/read
+    const long long cost = 64 * waves * per + (S > 1 ? (ctas * 2 * 8) / num_sms : 0);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = S;
+    }
+  }
+  return best;
+}
+
+int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
+  if (c.max_tokens > kMaxTokTiles * kTokTile) {
+    set_error("tcgen05 path supports max_tokens <= 64");
+    return PEARL_ERR_ARG;
+  }
+  int dev = 0;
+  PEARL_CUDA_TRY(cudaGetDevice(&dev));
+  PEARL_CUDA_TRY(cudaDeviceGetAttribute(&ctx.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  std::call_once(g_attr_once, [] {
+    g_attr_err = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kTcSmem));
+  });
+  PEARL_CUDA_TRY(g_attr_err);
+  ctx.max_tokens = c.max_tokens;
+  const int hd = c.head_dim;
+  const int shapes[5][2] = {{(c.n_heads + 2 * c.n_kv_heads) * hd, c.d_model},
+                            {c.d_model, c.n_heads * hd},
+                            {2 * c.ffn, c.d_model},
+                            {c.d_model, c.ffn},
+                            {c.vocab, c.d_model}};
+  size_t pf = 0;
+  int flags = 0;
+  for (auto& s : shapes) {
+    const int S = tc_splits(s[0], s[1], ctx.num_sms);
+    const int tiles = (s[0] + kTileN - 1) / kTileN;
+    pf = std::max(pf, static_cast<size_t>(tiles) * S * kTileN * kMaxTokTiles * kTokTile);
+    flags = std::max(flags, tiles);
+  }
+  ctx.partial_floats = pf;
+  ctx.n_flags = flags;
+  PEARL_CUDA_TRY(cudaMalloc(&ctx.partials, pf * sizeof(float)));
+  PEARL_CUDA_TRY(cudaMalloc(&ctx.tile_flags, static_cast<size_t>(flags) * sizeof(int)));
+  PEARL_CUDA_TRY(cudaMemset(ctx.tile_flags, 0, static_cast<size_t>(flags) * sizeof(int)));
+  return get_encoder();
+}
+
+void tc_free(TcGemmCtx& ctx) {
+  if (ctx.partials) cudaFree(ctx.partials);
+  if (ctx.tile_flags) cudaFree(ctx.tile_flags);
+  ctx.partials = nullptr;
+  ctx.tile_flags = nullptr;
+}
+
+int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int M, int N, int K, const EpiArgs& e,
+            cudaStream_t st, int force_splits) {
+  if (M < 1 || M > kMaxTokTiles * kTokTile) {
+    set_error("tc_gemm: M must be in [1, 64]");
+    return PEARL_ERR_ARG;
+  }
+  if (K % 8 != 0) {
+    set_error("tc_gemm: K must be a multiple of 8");
+    return PEARL_ERR_ARG;
+  }
+  auto it = ctx.wmaps.find(W);
+  if (it == ctx.wmaps.end()) {
+    TcWeightMap wm;
+    int rc = encode_2d(&wm.map, W, K, N, kTileN);
+    if (rc) return rc;
+    it = ctx.wmaps.emplace(W, wm).first;
+  }
+  alignas(64) CUtensorMap xmap;
+  int rc = encode_2d(&xmap, X, K, M, kTokTile);
+  if (rc) return rc;
+  TcArgs a;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.KB = (K + kTileK - 1) / kTileK;
+  a.S = force_splits > 0 ? force_splits : tc_splits(N, K, ctx.num_sms);
+  a.e = e;
+  a.partials = ctx.partials;
+  a.flags = ctx.tile_flags;
+  const int tiles = (N + kTileN - 1) / kTileN;
+  if (static_cast<size_t>(tiles) * a.S * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats || tiles > ctx.n_flags) {
+    set_error("tc_gemm: shape exceeds the planned split-K workspace");
+    return PEARL_ERR_ARG;
+  }
+  tc_gemm_kernel<<<tiles * a.S, kTcThreads, kTcSmem, st>>>(it->second.map, xmap, a);
+  PEARL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  return PEARL_OK;
+}
+
 }  // namespace pearl

@@ -20,10 +20,12 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "common.h"
+#include "epilogue.cuh"
 #include "gemm_tc.cuh"
 
 namespace pearl {
@@ -96,76 +98,6 @@ __global__ void rmsnorm_kernel(const float* __restrict__ h, const float* __restr
 }
 
 __global__ void advance_kernel(int32_t* pos, int n) { *pos += n; }
-
-// ---------------------------------------------------------------------------
-// Epilogues shared by the CUDA-core and tcgen05 GEMMs
-// ---------------------------------------------------------------------------
-enum EpiKind { EPI_STORE_F32 = 0, EPI_RESID = 1, EPI_QKV = 2, EPI_SWIGLU = 3 };
-
-struct EpiArgs {
-  int kind;
-  float* out_f32;   // STORE_F32: [M, N]; RESID: h [M, N]
-  bf16* out_bf16;   // QKV: q [M, H hd]; SWIGLU: act [M, N/2]
-  bf16* kc;         // QKV: layer k cache [max_seq, KV, hd]
-  bf16* vc;
-  const float* cos_t;
-  const float* sin_t;
-  const int32_t* pos;
-  int pos_add;
-  int n_q;          // H * hd
-  int n_kv;         // KV * hd
-  int hd;
-  int ld;           // leading dimension of out
-};
-
-// Handle four consecutive output rows n0..n0+3 (n0 % 4 == 0) for token t.
-__device__ __forceinline__ void epilogue4(const EpiArgs& e, int t, int n0, const float* v, int N) {
-  switch (e.kind) {
-    case EPI_STORE_F32:
-      for (int r = 0; r < 4; ++r)
-        if (n0 + r < N) e.out_f32[static_cast<size_t>(t) * e.ld + n0 + r] = v[r];
-      break;
-    case EPI_RESID:
-      for (int r = 0; r < 4; ++r)
-        if (n0 + r < N) e.out_f32[static_cast<size_t>(t) * e.ld + n0 + r] += v[r];
-      break;
-    case EPI_SWIGLU: {
-      // rows (2j, 2j+1) = (gate_j, up_j)
-      for (int r = 0; r < 4; r += 2) {
-        const float gt = v[r], up = v[r + 1];
-        const float s = gt / (1.0f + expf(-gt));
-        e.out_bf16[static_cast<size_t>(t) * e.ld + (n0 + r) / 2] = __float2bfloat16(s * up);
-      }
-      break;
-    }
-    case EPI_QKV: {
-      const int p = *e.pos + e.pos_add + t;
-      const int half = e.hd >> 1;
-      if (n0 < e.n_q + e.n_kv) {
-        float w[4];
-        for (int r = 0; r < 4; r += 2) {
-          const int n = n0 + r;
-          const int i = (n % e.hd) >> 1;  // rotation pair index within the head
-          const float c = e.cos_t[static_cast<size_t>(p) * half + i];
-          const float s = e.sin_t[static_cast<size_t>(p) * half + i];
-          w[r] = v[r] * c - v[r + 1] * s;
-          w[r + 1] = v[r] * s + v[r + 1] * c;
-        }
-        if (n0 < e.n_q) {
-          for (int r = 0; r < 4; ++r) e.out_bf16[static_cast<size_t>(t) * e.n_q + n0 + r] = __float2bfloat16(w[r]);
-        } else {
-          const int nk = n0 - e.n_q;
-          for (int r = 0; r < 4; ++r)
-            e.kc[static_cast<size_t>(p) * e.n_kv + nk + r] = __float2bfloat16(w[r]);
-        }
-      } else {
-        const int nv = n0 - e.n_q - e.n_kv;
-        for (int r = 0; r < 4; ++r) e.vc[static_cast<size_t>(p) * e.n_kv + nv + r] = __float2bfloat16(v[r]);
-      }
-      break;
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // K2: batch-invariant CUDA-core GEMV / skinny GEMM
@@ -466,6 +398,50 @@ extern "C" int pearl_llama_destroy(void* handle) {
   tc_free(m->tc);
   delete m;
   return PEARL_OK;
+}
+
+namespace {
+std::mutex g_gemm_mu;
+TcGemmCtx g_gemm_ctx;  // standalone pearl_gemm (tests / microbenchmarks)
+}  // namespace
+
+extern "C" int pearl_gemm(int kind, const void* W, const void* X, float* Y, int M, int N, int K, int splits,
+                          void* stream) {
+  PEARL_ARG_CHECK(W && X && Y && M >= 1 && N >= 1 && K >= 8, "bad gemm arguments");
+  EpiArgs e{};
+  e.kind = EPI_STORE_F32;
+  e.out_f32 = Y;
+  e.ld = N;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (kind == PEARL_GEMM_CUDACORE) {
+    const int rows_per_block = kGemvWarps * kGemvRows;
+    gemv_kernel<<<(N + rows_per_block - 1) / rows_per_block, kGemvWarps * 32, 0, st>>>(
+        static_cast<const bf16*>(W), static_cast<const bf16*>(X), M, N, K, e);
+    PEARL_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    return PEARL_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_gemm_mu);
+  if (!g_gemm_ctx.partials) {
+    pearl_llama_config c{};
+    c.n_layers = 1;
+    c.d_model = 8192;
+    c.n_heads = 64;
+    c.n_kv_heads = 8;
+    c.head_dim = 128;
+    c.ffn = 28672;
+    c.vocab = 131072;
+    c.max_tokens = 64;
+    int rc = tc_init(g_gemm_ctx, c);
+    if (rc) return rc;
+  }
+  return tc_gemm(g_gemm_ctx, static_cast<const bf16*>(W), static_cast<const bf16*>(X), M, N, K, e, st, splits);
+}
+
+extern "C" int pearl_gemm_splits(int N, int K) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return tc_splits(N, K, sms);
 }
 
 extern "C" size_t pearl_llama_workspace_bytes(void* handle, int n_tokens) {

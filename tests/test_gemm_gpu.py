@@ -1,0 +1,68 @@
+"""GPU: the two contraction engines (K2 CUDA-core GEMV, K3 tcgen05+TMA) vs a
+plain PyTorch fp32 reference of the same op, and their batch invariance."""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+SHAPES = [(128, 64), (300, 200), (2752, 512), (512, 1376), (4096, 4096), (12288, 4096), (32000, 768),
+          (4096, 11008), (1000, 72)]
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2408_11850_b200 import _lib
+    return _lib
+
+
+def _gemm(lib, kind, W, X, splits=0):
+    M, K = X.shape
+    N = W.shape[0]
+    Y = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    lib.check(lib.load().pearl_gemm(kind, W.data_ptr(), X.data_ptr(), Y.data_ptr(), M, N, K, splits,
+                                    torch.cuda.current_stream().cuda_stream), "pearl_gemm")
+    torch.cuda.synchronize()
+    return Y
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("N,K", SHAPES)
+def test_matches_fp32_reference(lib, kind, N, K):
+    g = torch.Generator(device="cuda").manual_seed(N * 7 + K)
+    W = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    for M in (1, 3, 16, 17, 40, 64):
+        X = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+        Y = _gemm(lib, kind, W, X)
+        ref = X.float() @ W.float().T
+        tol = 2e-5 * K ** 0.5 + 1e-4 * ref.abs().max().item()
+        assert torch.isfinite(Y).all()
+        assert (Y - ref).abs().max().item() <= tol, (kind, N, K, M, (Y - ref).abs().max().item())
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_batch_invariance(lib, kind):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for N, K in [(4096, 4096), (300, 1376), (32000, 768)]:
+        W = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+        X = torch.randn(64, K, generator=g, device="cuda").to(torch.bfloat16)
+        full = _gemm(lib, kind, W, X)
+        for M in (1, 2, 5, 16, 33):
+            part = _gemm(lib, kind, W, X[:M].contiguous())
+            assert torch.equal(part, full[:M]), (kind, N, K, M)
+        # a token's row does not depend on the other rows' values either
+        X2 = X.clone()
+        X2[1:] = torch.randn_like(X2[1:].float()).to(torch.bfloat16)
+        assert torch.equal(_gemm(lib, kind, W, X2)[0], full[0])
+
+
+def test_split_k_is_deterministic_and_close(lib):
+    g = torch.Generator(device="cuda").manual_seed(9)
+    W = (torch.randn(4096, 11008, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    X = torch.randn(8, 11008, generator=g, device="cuda").to(torch.bfloat16)
+    a = _gemm(lib, 1, W, X)
+    assert torch.equal(a, _gemm(lib, 1, W, X))
+    b = _gemm(lib, 1, W, X, splits=1)
+    assert (a - b).abs().max().item() < 1e-2
