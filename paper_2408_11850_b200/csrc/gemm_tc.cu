@@ -354,12 +354,13 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
     set_error("tc_gemm: K must be a multiple of 8");
     return PEARL_ERR_ARG;
   }
-  auto it = ctx.wmaps.find(W);
+  const auto key = std::make_tuple(static_cast<const void*>(W), N, K);
+  auto it = ctx.wmaps.find(key);
   if (it == ctx.wmaps.end()) {
     TcWeightMap wm;
     int rc = encode_2d(&wm.map, W, K, N, kTileN);
     if (rc) return rc;
-    it = ctx.wmaps.emplace(W, wm).first;
+    it = ctx.wmaps.emplace(key, wm).first;
   }
   alignas(64) CUtensorMap xmap;
   int rc = encode_2d(&xmap, X, K, M, kTokTile);

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <tuple>
 
 #include "common.h"
 
@@ -32,7 +33,8 @@ struct TcGemmCtx {
   int n_flags = 0;
   int max_tokens = 0;
   int num_sms = 148;
-  std::map<const void*, TcWeightMap> wmaps;  // per weight matrix
+  // per weight matrix, keyed by (address, N, K): a map encodes the shape too
+  std::map<std::tuple<const void*, int, int>, TcWeightMap> wmaps;
 };
 
 int tc_init(TcGemmCtx& ctx, const pearl_llama_config& cfg);

@@ -22,12 +22,13 @@ LOGIT_ATOL_BF16_POINTS = 5e-2   # oracle rounds to bf16 at the same points
 LOGIT_RTOL = 1e-2
 
 
-@pytest.fixture(scope="module")
-def pair():
+@pytest.fixture(scope="module", params=["tcgen05", "cudacore"])
+def pair(request):
+    """tiny pair; the target runs on the tcgen05 engine (K3) or the CUDA-core GEMV (K2)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2408_11850_b200 import llama
-    target, draft = llama.build_pair("tiny", max_seq=512, max_tokens=32)
+    target, draft = llama.build_pair("tiny", gemm_target=request.param, max_seq=512, max_tokens=32)
     return target, draft
 
 
