@@ -1,14 +1,25 @@
 // K3: tcgen05 + TMA small-M contraction (see gemm_tc.cuh).
 //
-// CTA = 4 warps, one (row tile, K split) unit:
-//   warp 0 / lane 0 : TMA producer -- 128x64 W tile + NT 16x64 X tiles per
-//                     stage into a kStages-deep smem ring (SWIZZLE_128B)
+// Persistent, warp-specialised CTA (one per SM), 6 warps:
+//   warp 0 / lane 0 : TMA producer.  Streams the 128x64 W tile and the NT
+//                     16x64 X tiles of every k-block of every work unit the
+//                     CTA owns into a multi-stage smem ring (SWIZZLE_128B),
+//                     running ahead across unit boundaries.  W tiles of the
+//                     first stages are requested before griddepcontrol.wait
+//                     (PDL), i.e. while the previous kernel is still running.
 //   warp 1          : TMEM allocator; lane 0 issues tcgen05.mma
-//                     (M=128, N=16, K=16, bf16 -> fp32) and tcgen05.commit
-//                     releases each smem stage back to the producer
-//   all 4 warps     : epilogue -- tcgen05.ld 32x32b (warp w owns TMEM lanes
-//                     32w..32w+31 = weight rows), fixed-order split-K sum by
-//                     the last-arriving CTA, then the shared fused epilogue.
+//                     (M=128 weight rows, N=16 tokens, K=16, bf16 -> fp32)
+//                     into one of two TMEM accumulators and tcgen05.commit
+//                     releases smem stages / publishes finished units.
+//   warps 2..5      : epilogue.  tcgen05.ld 32x32b (warp w owns TMEM lanes
+//                     32(w%4)..+31 = weight rows), frees the accumulator for
+//                     the unit after next, then either applies the fused
+//                     epilogue (no split) or stores an fp32 partial; the last
+//                     CTA to finish a row tile sums its partials in split
+//                     order and applies the epilogue.
+// Work unit = (row tile, K split); the split count is a function of (N, K)
+// only and units are assigned round-robin, so every output element is the
+// same fp32 computation whatever the number of tokens M (batch invariance).
 #include "gemm_tc.cuh"
 
 #include <cuda.h>
@@ -22,19 +33,21 @@
 
 namespace pearl {
 
-constexpr int kTcStages = 6;
 constexpr int kTileN = 128;    // weight rows per tile (MMA-M)
 constexpr int kTileK = 64;     // K per stage (one 128-byte swizzle row)
 constexpr int kTokTile = 16;   // tokens per MMA (MMA-N)
 constexpr int kMaxTokTiles = 4;
-constexpr int kWBytes = kTileN * kTileK * 2;        // 16 KB
-constexpr int kXBytes = kTokTile * kTileK * 2;      // 2 KB per token tile
-constexpr int kStageBytes = kWBytes + kMaxTokTiles * kXBytes;  // 24 KB
-constexpr int kTcThreads = 128;
-constexpr size_t kTcSmem = 1024 /*align slack*/ + static_cast<size_t>(kTcStages) * kStageBytes + 256;
+constexpr int kWBytes = kTileN * kTileK * 2;   // 16 KB
+constexpr int kXBytes = kTokTile * kTileK * 2; // 2 KB per token tile
+constexpr int kRingBytes = 144 * 1024;         // smem ring (stages sized by NT)
+constexpr int kMaxStages = 8;
+constexpr int kEBytes = kTileN * 64 * 4;       // epilogue staging [128][64] fp32
+constexpr int kTcThreads = 192;
+constexpr int kEpiThreads = 128;
+constexpr size_t kTcSmem = 1024 + kRingBytes + kEBytes + 512;
 
 struct TcArgs {
-  int M, N, K, KB, S;
+  int M, N, K, KB, S, units;
   EpiArgs e;
   float* partials;
   int* flags;
@@ -52,6 +65,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
@@ -110,132 +127,198 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
+
+__device__ __forceinline__ void unit_range(const TcArgs& a, int u, int& tile, int& split, int& kb0, int& kb1) {
+  tile = u / a.S;
+  split = u % a.S;
+  kb0 = static_cast<int>((static_cast<long long>(split) * a.KB) / a.S);
+  kb1 = static_cast<int>((static_cast<long long>(split + 1) * a.KB) / a.S);
+}
+
 // ---- kernel ------------------------------------------------------------------
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcArgs a) {
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
-  // 1024-byte alignment for SWIZZLE_128B
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * kStageBytes);
-  uint64_t* empty = full + kTcStages;
-  uint64_t* accum = empty + kTcStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-  __shared__ int s_last;
+  float* E = reinterpret_cast<float*>(smem + kRingBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kEBytes);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* acc_full = empty + kMaxStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x / a.S;
-  const int split = blockIdx.x % a.S;
-  const int kb0 = static_cast<int>((static_cast<long long>(split) * a.KB) / a.S);
-  const int kb1 = static_cast<int>((static_cast<long long>(split + 1) * a.KB) / a.S);
-  const int nkb = kb1 - kb0;
   const int NT = (a.M + kTokTile - 1) / kTokTile;
+  const int stage_bytes = kWBytes + NT * kXBytes;
+  const int stages = min(kMaxStages, kRingBytes / stage_bytes);
+  // units of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
+  const int my_units = a.units > static_cast<int>(blockIdx.x) ? (a.units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kEpiThreads);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
   }
   if (warp == 1) {
-    // 64 fp32 columns: up to 4 token tiles of 16
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tmem_slot)));
+    // two accumulators x 64 fp32 columns (up to 4 token tiles of 16)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // every CTA of this persistent grid is resident: dependents may launch now
+  // (they block in griddepcontrol.wait until this grid has completed)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer
-    const uint32_t bytes = kWBytes + NT * kXBytes;
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % kTcStages;
-      if (i >= kTcStages) mbar_wait(&empty[s], ((i / kTcStages) - 1) & 1);
-      unsigned char* st = smem + s * kStageBytes;
-      mbar_expect_tx(&full[s], bytes);
-      const int kc = (kb0 + i) * kTileK;
-      tma_load_2d(st, &tmW, &full[s], kc, tile * kTileN);
-      for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % kTcStages;
-      mbar_wait(&full[s], (i / kTcStages) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      unsigned char* st = smem + s * kStageBytes;
-      const uint64_t adesc = umma_desc_sw128(st);
-      for (int j = 0; j < NT; ++j) {
-        const uint64_t bdesc = umma_desc_sw128(st + kWBytes + j * kXBytes);
-#pragma unroll
-        for (int kk = 0; kk < kTileK / 16; ++kk) {
-          // advance 16 bf16 = 32 bytes along K inside the swizzle row
-          umma_bf16(tmem + j * kTokTile, adesc + 2 * kk, bdesc + 2 * kk, (i > 0 || kk > 0) ? 1u : 0u);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer: iteration it walks (unit, k-block) in order
+      int total = 0;
+      for (int ui = 0; ui < my_units; ++ui) {
+        int t, sp, k0, k1;
+        unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
+        total += k1 - k0;
+      }
+      const uint32_t bytes = stage_bytes;
+      const int npre = min(stages, total);
+      // W does not depend on the previous kernel: request it before the PDL wait
+      int ui = 0, t = 0, sp = 0, k0 = 0, k1 = 0, kb = 0;
+      if (my_units > 0) {
+        unit_range(a, blockIdx.x, t, sp, k0, k1);
+        kb = k0;
+      }
+      int pre_k[kMaxStages];
+      for (int it = 0; it < npre; ++it) {
+        unsigned char* st = smem + it * stage_bytes;
+        mbar_expect_tx(&full[it], bytes);
+        tma_load_2d(st, &tmW, &full[it], kb * kTileK, t * kTileN);
+        pre_k[it] = kb;
+        if (++kb == k1 && ++ui < my_units) {
+          unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
+          kb = k0;
         }
       }
-      umma_commit(&empty[s]);
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int it = 0; it < npre; ++it) {
+        unsigned char* st = smem + it * stage_bytes;
+        for (int j = 0; j < NT; ++j)
+          tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[it], pre_k[it] * kTileK, j * kTokTile);
+      }
+      for (int it = npre; it < total; ++it) {
+        const int s = it % stages;
+        mbar_wait(&empty[s], ((it / stages) - 1) & 1);
+        unsigned char* st = smem + s * stage_bytes;
+        mbar_expect_tx(&full[s], bytes);
+        tma_load_2d(st, &tmW, &full[s], kb * kTileK, t * kTileN);
+        for (int j = 0; j < NT; ++j)
+          tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kb * kTileK, j * kTokTile);
+        if (++kb == k1 && ++ui < my_units) {
+          unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
+          kb = k0;
+        }
+      }
     }
-    umma_commit(accum);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer
+      int it = 0;
+      for (int ui = 0; ui < my_units; ++ui) {
+        int t, sp, k0, k1;
+        unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
+        const int b = ui & 1;
+        if (ui >= 2) mbar_wait(&acc_empty[b], ((ui >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + b * 64;
+        for (int kb = k0; kb < k1; ++kb, ++it) {
+          const int s = it % stages;
+          mbar_wait(&full[s], (it / stages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          unsigned char* st = smem + s * stage_bytes;
+          const uint64_t adesc = umma_desc_sw128(st);
+          for (int j = 0; j < NT; ++j) {
+            const uint64_t bdesc = umma_desc_sw128(st + kWBytes + j * kXBytes);
+#pragma unroll
+            for (int kk = 0; kk < kTileK / 16; ++kk)
+              umma_bf16(acc + j * kTokTile, adesc + 2 * kk, bdesc + 2 * kk, (kb > k0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[b]);
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5
+    const int lanegrp = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = lanegrp * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
+    const int TOKP = NT * kTokTile;
+    for (int ui = 0; ui < my_units; ++ui) {
+      int tile, split, k0, k1;
+      unit_range(a, blockIdx.x + ui * gridDim.x, tile, split, k0, k1);
+      const int b = ui & 1;
+      mbar_wait(&acc_full[b], (ui >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float v[kMaxTokTiles][16];
+      for (int j = 0; j < NT; ++j)
+        tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * 64 + j * kTokTile, v[j]);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acc_empty[b]);  // the MMA warp may reuse this accumulator
+      if (a.S == 1) {
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int c = 0; c < 16; ++c) E[row * 64 + j * 16 + c] = v[j][c];
+      } else {
+        float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * TOKP;
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int c = 0; c < 16; c += 4)
+            *reinterpret_cast<float4*>(dst + j * 16 + c) = make_float4(v[j][c], v[j][c + 1], v[j][c + 2], v[j][c + 3]);
+        __threadfence();
+        epi_bar();
+        if (et == 0) *s_last = (atomicAdd(&a.flags[tile], 1) == a.S - 1);
+        epi_bar();
+        if (!*s_last) continue;
+        __threadfence();
+        // fixed split order => independent of arrival order and of M
+        for (int t = 0; t < a.M; ++t) {
+          float acc = 0.f;
+          for (int s = 0; s < a.S; ++s)
+            acc += __ldcg(a.partials + ((static_cast<size_t>(tile) * a.S + s) * kTileN + row) * TOKP + t);
+          E[row * 64 + t] = acc;
+        }
+        if (et == 0) a.flags[tile] = 0;
+      }
+      epi_bar();
+      const int groups = kTileN / 4;
+      for (int idx = et; idx < groups * a.M; idx += kEpiThreads) {
+        const int g = idx % groups, t = idx / groups;
+        const int n0 = tile * kTileN + g * 4;
+        if (n0 >= a.N) continue;
+        float w[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) w[r] = E[(g * 4 + r) * 64 + t];
+        epilogue4(a.e, t, n0, w, a.N);
+      }
+      epi_bar();
+    }
   }
   __syncwarp();
-  // ---- epilogue (all warps)
-  mbar_wait(accum, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  float* E = reinterpret_cast<float*>(smem);  // [128][64] fp32 staging, reuses the ring
-  const int row = warp * 32 + lane;
-  const int TOKP = NT * kTokTile;
-  float v[16];
-  for (int j = 0; j < NT; ++j) {
-    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + j * kTokTile, v);
-    if (a.S == 1) {
-#pragma unroll
-      for (int c = 0; c < 16; ++c) E[row * 64 + j * 16 + c] = v[c];
-    } else {
-      float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * TOKP + j * kTokTile;
-#pragma unroll
-      for (int c = 0; c < 16; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-    }
-  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  if (a.S > 1) {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&a.flags[tile], 1) == a.S - 1);
-    __syncthreads();
-    if (!s_last) {
-      if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
-      return;
-    }
-    __threadfence();
-    // fixed split order => result independent of arrival order and of M
-    for (int t = 0; t < a.M; ++t) {
-      float acc = 0.f;
-      for (int s = 0; s < a.S; ++s)
-        acc += __ldcg(a.partials + ((static_cast<size_t>(tile) * a.S + s) * kTileN + row) * TOKP + t);
-      E[row * 64 + t] = acc;
-    }
-    if (threadIdx.x == 0) a.flags[tile] = 0;
-  }
   __syncthreads();
-  // fused epilogue over (4-row group, token)
-  const int groups = kTileN / 4;
-  for (int idx = threadIdx.x; idx < groups * a.M; idx += blockDim.x) {
-    const int g = idx % groups, t = idx / groups;
-    const int n0 = tile * kTileN + g * 4;
-    if (n0 >= a.N) continue;
-    float w[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) w[r] = E[(g * 4 + r) * 64 + t];
-    epilogue4(a.e, t, n0, w, a.N);
-  }
-  __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -281,19 +364,22 @@ cudaError_t g_attr_err = cudaSuccess;
 
 }  // namespace
 
+// Split-K factor for an (N, K) weight: enough (tile, split) units to keep
+// every SM's pipeline busy while per-SM work stays balanced.  Depends on the
+// shape only (batch invariance).
 int tc_splits(int N, int K, int num_sms) {
   const int tiles = (N + kTileN - 1) / kTileN;
   const int KB = (K + kTileK - 1) / kTileK;
   int best = 1;
-  long long best_cost = -1;
+  double best_cost = -1;
   for (int S = 1; S <= std::min(KB, 32); ++S) {
-    if (KB / S < 4 && S > 1) break;  // keep >= 4 k-blocks of streaming per CTA
-    const long long ctas = static_cast<long long>(tiles) * S;
-    const long long waves = (ctas + num_sms - 1) / num_sms;
-    const long long per = (KB + S - 1) / S;
-    // per-SM streamed k-blocks + a small cost per partial tile written/read
-    const long long cost = 64 * waves * per + (S > 1 ? (ctas * 2 * 8) / num_sms : 0);
-    if (best_cost < 0 || cost < best_cost) {
+    if (KB / S < 4 && S > 1) break;  // keep >= 4 k-blocks of streaming per unit
+    const long long units = static_cast<long long>(tiles) * S;
+    // persistent round-robin: the busiest SM streams ceil(units/sms) units of
+    // ceil(KB/S) blocks; splitting also costs partial-tile traffic
+    const double per_sm = static_cast<double>((units + num_sms - 1) / num_sms) * ((KB + S - 1) / S);
+    const double cost = per_sm + (S > 1 ? 0.15 * static_cast<double>(units) * 2.0 / num_sms : 0.0);
+    if (best_cost < 0 || cost < best_cost - 1e-9) {
       best_cost = cost;
       best = S;
     }
@@ -375,12 +461,22 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;
   const int tiles = (N + kTileN - 1) / kTileN;
+  a.units = tiles * a.S;
   if (static_cast<size_t>(tiles) * a.S * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats || tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");
     return PEARL_ERR_ARG;
   }
-  tc_gemm_kernel<<<tiles * a.S, kTcThreads, kTcSmem, st>>>(it->second.map, xmap, a);
-  PEARL_CUDA_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(a.units, ctx.num_sms));
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = kTcSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel, it->second.map, xmap, a));
   count_launch();
   return PEARL_OK;
 }

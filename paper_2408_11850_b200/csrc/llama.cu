@@ -7,21 +7,27 @@
 // positions *pos..*pos+n-1 against the per-layer KV cache.
 //
 // Layer = RMSNorm -> QKV GEMM (+RoPE, +K/V append) -> causal attention over
-// the cache -> O GEMM (+residual) -> RMSNorm -> gate/up GEMM (+SwiGLU) ->
-// down GEMM (+residual).  The residual stream is fp32; GEMM operands bf16.
+// the cache (K4) -> O GEMM (+residual) -> RMSNorm -> gate/up GEMM (+SwiGLU)
+// -> down GEMM (+residual).  The residual stream is fp32; GEMM operands bf16.
+// Every kernel is launched with programmatic dependent launch (PDL): it may
+// start while its predecessor drains and calls griddepcontrol.wait before
+// touching the predecessor's outputs (the tcgen05 GEMM prefetches weights
+// before that wait).
 //
 // Batch invariance: every per-token value is computed by the same sequence
 // of fp32 operations whatever the number of tokens in the launch (fixed
-// K-order FMA chains, fixed shuffle trees, per-(token, head) attention with
-// a sequential softmax-weighted sum), so a position's logits are bitwise the
-// same in an M=1 AR step, an M=gamma PEARL window or an M=gamma+1 SD window.
-// That property is what makes GPU greedy PEARL/SD token-identical to GPU AR.
+// K-order FMA chains, fixed reduction trees, per-(token, head) attention with
+// fixed 64-position chunks combined in chunk order), so a position's logits
+// are bitwise the same in an M=1 AR step, an M=gamma PEARL window or an
+// M=gamma+1 SD window -- which makes GPU greedy PEARL/SD token-identical to AR.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.h"
@@ -29,8 +35,6 @@
 #include "gemm_tc.cuh"
 
 namespace pearl {
-
-using bf16 = __nv_bfloat16;
 
 struct LayerW {
   const float* attn_norm;
@@ -40,6 +44,8 @@ struct LayerW {
   const bf16* wgu;
   const bf16* wdown;
 };
+
+constexpr int kAttnChunk = 64;  // positions per attention work item
 
 struct Llama {
   pearl_llama_config cfg;
@@ -57,14 +63,39 @@ struct Llama {
   bf16* q = nullptr;      // [T, H hd]
   bf16* o = nullptr;      // [T, H hd]
   bf16* act = nullptr;    // [T, ffn]
+  float* attn_part = nullptr;  // [T, H, chunks, hd + 2] partial (m, l, o)
+  int* attn_flags = nullptr;   // [H] arrival counters (self-resetting)
+  int max_chunks = 0;
   TcGemmCtx tc;           // tcgen05 path state (split-K scratch, descriptors)
 };
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  count_launch();
+  return PEARL_OK;
+}
 
 // ---------------------------------------------------------------------------
 // small kernels
 // ---------------------------------------------------------------------------
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const bf16* __restrict__ emb, float* __restrict__ h,
                              int d, int V) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   int tok = tokens[t];
   tok = tok < 0 ? 0 : (tok >= V ? V - 1 : tok);
@@ -76,6 +107,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const bf16* __r
 // fixed reduction order.
 __global__ void rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g, bf16* __restrict__ x,
                                int d, float eps, int row_off) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x + row_off;
   const float* hr = h + static_cast<size_t>(t) * d;
   float ss = 0.f;
@@ -97,7 +130,10 @@ __global__ void rmsnorm_kernel(const float* __restrict__ h, const float* __restr
   for (int i = threadIdx.x; i < d; i += blockDim.x) xr[i] = __float2bfloat16(hr[i] * rs * g[i]);
 }
 
-__global__ void advance_kernel(int32_t* pos, int n) { *pos += n; }
+__global__ void advance_kernel(int32_t* pos, int n) {
+  pdl_wait();
+  *pos += n;
+}
 
 // ---------------------------------------------------------------------------
 // K2: batch-invariant CUDA-core GEMV / skinny GEMM
@@ -129,6 +165,8 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
 
 __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __restrict__ W, const bf16* __restrict__ X,
                                                                int M, int N, int K, EpiArgs e) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = (blockIdx.x * kGemvWarps + warp) * kGemvRows;
   if (n0 >= N) return;
@@ -179,73 +217,133 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
 }
 
 // ---------------------------------------------------------------------------
-// K4: causal attention of the window's queries over the cache
-//   one block per (head, token); scores in smem; softmax and the weighted
-//   value sum in a fixed order, so the result depends only on the token's
-//   own position and the cache contents.
+// K4: causal attention of the window's M queries over the KV cache.
+// Work item = (query head h, 64-position chunk c).  A block stages the
+// chunk's K and V rows of h's KV head in shared memory and, for every window
+// token t whose causal range reaches the chunk, computes fixed-order dot
+// products, the chunk's max / sum-of-exp and the exp-weighted V sum.  The
+// last block to finish head h combines the chunks of each token in chunk
+// order.  Each token's result therefore depends only on its own position and
+// the cache contents (batch invariance).
 // ---------------------------------------------------------------------------
-__global__ void attention_kernel(const bf16* __restrict__ q, const bf16* __restrict__ kc, const bf16* __restrict__ vc,
-                                 bf16* __restrict__ o, const int32_t* pos, int pos_add, int H, int KV, int hd,
-                                 float scale) {
-  extern __shared__ float sc[];
-  __shared__ float red[32];
-  const int h = blockIdx.x, t = blockIdx.y;
-  const int kvh = h / (H / KV);
-  const int ctx = *pos + pos_add + t + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int per = hd / 32;  // 2 or 4
-  float qv[4];
-  const bf16* qr = q + (static_cast<size_t>(t) * H + h) * hd;
-  for (int i = 0; i < per; ++i) qv[i] = __bfloat162float(qr[lane * per + i]);
-  const size_t kstride = static_cast<size_t>(KV) * hd;
-  for (int j = warp; j < ctx; j += nw) {
-    const bf16* kr = kc + j * kstride + kvh * hd + lane * per;
-    float s = 0.f;
-    for (int i = 0; i < per; ++i) s = fmaf(qv[i], __bfloat162float(kr[i]), s);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) sc[j] = s * scale;
+struct AttnArgs {
+  const bf16* q;      // [M, H, hd]
+  const bf16* kc;     // layer cache [max_seq, KV, hd]
+  const bf16* vc;
+  bf16* o;            // [M, H, hd]
+  float* part;        // [T, H, chunks, hd + 2]
+  int* flags;         // [H]
+  const int32_t* pos;
+  int pos_add, M, H, KV, hd, max_chunks;
+  float scale;
+};
+
+__global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
+  extern __shared__ __align__(16) unsigned char attn_smem[];
+  __shared__ int s_last;
+  pdl_wait();
+  pdl_trigger();
+  const int h = blockIdx.x, c = blockIdx.y;
+  const int hd = a.hd;
+  const int p0 = *a.pos + a.pos_add;          // position of window token 0
+  const int ctx_max = p0 + a.M;               // positions 0 .. ctx_max-1 exist
+  const int n_chunks = (ctx_max + kAttnChunk - 1) / kAttnChunk;
+  if (c >= n_chunks) return;                  // not part of this launch's work
+  const int kvh = h / (a.H / a.KV);
+  const int j0 = c * kAttnChunk;
+  const int nj = min(kAttnChunk, ctx_max - j0);
+  // tokens whose causal range reaches this chunk: pos_t = p0 + t >= j0
+  const int t_first = max(0, j0 - p0);
+  const int nt = a.M - t_first;
+  bf16* Ks = reinterpret_cast<bf16*>(attn_smem);                 // [64][hd]
+  bf16* Vs = Ks + kAttnChunk * hd;                                // [64][hd]
+  float* S = reinterpret_cast<float*>(Vs + kAttnChunk * hd);      // [nt][64]
+  float* stats = S + nt * kAttnChunk;                             // [nt][2]
+  const size_t kstride = static_cast<size_t>(a.KV) * hd;
+  // stage K / V rows (16-byte vectors)
+  const int vec_per_row = hd / 8;
+  for (int i = threadIdx.x; i < nj * vec_per_row; i += blockDim.x) {
+    const int j = i / vec_per_row, v = i % vec_per_row;
+    const size_t g = (j0 + j) * kstride + kvh * hd + v * 8;
+    reinterpret_cast<uint4*>(Ks + j * hd)[v] = *reinterpret_cast<const uint4*>(a.kc + g);
+    reinterpret_cast<uint4*>(Vs + j * hd)[v] = *reinterpret_cast<const uint4*>(a.vc + g);
   }
   __syncthreads();
-  // max
-  float m = -INFINITY;
-  for (int j = threadIdx.x; j < ctx; j += blockDim.x) m = fmaxf(m, sc[j]);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if (lane == 0) red[warp] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float mm = -INFINITY;
-    for (int w = 0; w < nw; ++w) mm = fmaxf(mm, red[w]);
-    red[31] = mm;
+  // scores: one thread per (token, position); fixed sequential dot over hd
+  for (int i = threadIdx.x; i < nt * kAttnChunk; i += blockDim.x) {
+    const int t = t_first + i / kAttnChunk, j = i % kAttnChunk;
+    float s = -INFINITY;
+    if (j < nj && j0 + j <= p0 + t) {
+      const bf16* qr = a.q + (static_cast<size_t>(t) * a.H + h) * hd;
+      const bf16* kr = Ks + j * hd;
+      float acc = 0.f;
+      for (int d = 0; d < hd; d += 2) {
+        const __nv_bfloat162 q2 = *reinterpret_cast<const __nv_bfloat162*>(qr + d);
+        const __nv_bfloat162 k2 = *reinterpret_cast<const __nv_bfloat162*>(kr + d);
+        acc = fmaf(__low2float(q2), __low2float(k2), acc);
+        acc = fmaf(__high2float(q2), __high2float(k2), acc);
+      }
+      s = acc * a.scale;
+    }
+    S[i] = s;
   }
   __syncthreads();
-  m = red[31];
-  __syncthreads();
-  float sum = 0.f;
-  for (int j = threadIdx.x; j < ctx; j += blockDim.x) {
-    const float p = expf(sc[j] - m);
-    sc[j] = p;
-    sum += p;
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-  if (lane == 0) red[warp] = sum;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float ss = 0.f;
-    for (int w = 0; w < nw; ++w) ss += red[w];
-    red[30] = ss;
+  // per-token chunk max and sum of exp (sequential over the chunk)
+  for (int tt = threadIdx.x; tt < nt; tt += blockDim.x) {
+    const float* st = S + tt * kAttnChunk;
+    float m = -INFINITY;
+    for (int j = 0; j < kAttnChunk; ++j) m = fmaxf(m, st[j]);
+    float l = 0.f;
+    for (int j = 0; j < kAttnChunk; ++j) l += (st[j] == -INFINITY) ? 0.f : expf(st[j] - m);
+    stats[2 * tt] = m;
+    stats[2 * tt + 1] = l;
   }
   __syncthreads();
-  const float inv = 1.0f / red[30];
-  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-    const bf16* vr = vc + kvh * hd + d;
+  // exp-weighted V sum per (token, dim), sequential over the chunk
+  for (int i = threadIdx.x; i < nt * hd; i += blockDim.x) {
+    const int tt = i / hd, d = i % hd;
+    const float* st = S + tt * kAttnChunk;
+    const float m = stats[2 * tt];
     float acc = 0.f;
-#pragma unroll 8
-    for (int j = 0; j < ctx; ++j) acc = fmaf(sc[j], __bfloat162float(vr[j * kstride]), acc);
-    o[(static_cast<size_t>(t) * H + h) * hd + d] = __float2bfloat16(acc * inv);
+    for (int j = 0; j < nj; ++j) {
+      const float s = st[j];
+      if (s != -INFINITY) acc = fmaf(expf(s - m), __bfloat162float(Vs[j * hd + d]), acc);
+    }
+    float* pr = a.part + ((static_cast<size_t>(t_first + tt) * a.H + h) * a.max_chunks + c) * (hd + 2);
+    pr[2 + d] = acc;
+    if (d == 0) {
+      pr[0] = m;
+      pr[1] = stats[2 * tt + 1];
+    }
   }
+  // last block of head h combines
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&a.flags[h], 1) == n_chunks - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < a.M * hd; i += blockDim.x) {
+    const int t = i / hd, d = i % hd;
+    const int nc = (p0 + t) / kAttnChunk + 1;  // chunks covering 0..p0+t
+    const float* pt = a.part + (static_cast<size_t>(t) * a.H + h) * a.max_chunks * (hd + 2);
+    float mx = -INFINITY;
+    for (int cc = 0; cc < nc; ++cc) mx = fmaxf(mx, __ldcg(pt + cc * (hd + 2)));
+    float L = 0.f, O = 0.f;
+    for (int cc = 0; cc < nc; ++cc) {
+      const float* pc = pt + cc * (hd + 2);
+      const float w = expf(__ldcg(pc) - mx);
+      L = fmaf(w, __ldcg(pc + 1), L);
+      O = fmaf(w, __ldcg(pc + 2 + d), O);
+    }
+    a.o[(static_cast<size_t>(t) * a.H + h) * hd + d] = __float2bfloat16(O / L);
+  }
+  if (threadIdx.x == 0) a.flags[h] = 0;
+}
+
+size_t attention_smem_bytes(int T, int hd) {
+  return static_cast<size_t>(2) * kAttnChunk * hd * sizeof(bf16) + static_cast<size_t>(T) * kAttnChunk * 4 +
+         static_cast<size_t>(T) * 2 * 4 + 16;
 }
 
 // ---------------------------------------------------------------------------
@@ -253,13 +351,15 @@ __global__ void attention_kernel(const bf16* __restrict__ q, const bf16* __restr
 // ---------------------------------------------------------------------------
 namespace {
 
+int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st) {
+  const int rows_per_block = kGemvWarps * kGemvRows;
+  return launch_pdl(gemv_kernel, dim3((N + rows_per_block - 1) / rows_per_block), dim3(kGemvWarps * 32), 0, st, W, X,
+                    M, N, K, e);
+}
+
 int launch_gemm(Llama& m, const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st) {
   if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st);
-  const int rows_per_block = kGemvWarps * kGemvRows;
-  gemv_kernel<<<(N + rows_per_block - 1) / rows_per_block, kGemvWarps * 32, 0, st>>>(W, X, M, N, K, e);
-  PEARL_CUDA_TRY(cudaGetLastError());
-  count_launch();
-  return PEARL_OK;
+  return launch_gemv(W, X, M, N, K, e, st);
 }
 
 int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_add, bool logits_all,
@@ -267,18 +367,15 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   const auto& c = m.cfg;
   const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads;
   const int nq = H * hd, nkv = KV * hd;
-  embed_kernel<<<M, 256, 0, st>>>(tokens, m.embed, m.h, d, c.vocab);
-  PEARL_CUDA_TRY(cudaGetLastError());
-  count_launch();
+  int rc = launch_pdl(embed_kernel, dim3(M), dim3(256), 0, st, tokens, m.embed, m.h, d, c.vocab);
+  if (rc) return rc;
   const size_t layer_kv = static_cast<size_t>(c.max_seq) * nkv;
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
-  const int attn_threads = 128;
-  const size_t attn_smem = static_cast<size_t>(c.max_seq) * sizeof(float);
+  const size_t attn_smem = attention_smem_bytes(M, hd);
   for (int l = 0; l < c.n_layers; ++l) {
     const LayerW& L = m.layers[l];
-    rmsnorm_kernel<<<M, 256, 0, st>>>(m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
-    PEARL_CUDA_TRY(cudaGetLastError());
-    count_launch();
+    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
+    if (rc) return rc;
     EpiArgs e{};
     e.kind = EPI_QKV;
     e.out_bf16 = m.q;
@@ -291,21 +388,19 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     e.n_q = nq;
     e.n_kv = nkv;
     e.hd = hd;
-    int rc = launch_gemm(m, L.wqkv, m.x, M, nq + 2 * nkv, d, e, st);
+    rc = launch_gemm(m, L.wqkv, m.x, M, nq + 2 * nkv, d, e, st);
     if (rc) return rc;
-    attention_kernel<<<dim3(H, M), attn_threads, attn_smem, st>>>(m.q, e.kc, e.vc, m.o, pos, pos_add, H, KV, hd,
-                                                                  scale);
-    PEARL_CUDA_TRY(cudaGetLastError());
-    count_launch();
+    AttnArgs aa{m.q, e.kc, e.vc, m.o, m.attn_part, m.attn_flags, pos, pos_add, M, H, KV, hd, m.max_chunks, scale};
+    rc = launch_pdl(attention_kernel, dim3(H, m.max_chunks), dim3(128), attn_smem, st, aa);
+    if (rc) return rc;
     EpiArgs r{};
     r.kind = EPI_RESID;
     r.out_f32 = m.h;
     r.ld = d;
     rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
     if (rc) return rc;
-    rmsnorm_kernel<<<M, 256, 0, st>>>(m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
-    PEARL_CUDA_TRY(cudaGetLastError());
-    count_launch();
+    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
+    if (rc) return rc;
     EpiArgs g{};
     g.kind = EPI_SWIGLU;
     g.out_bf16 = m.act;
@@ -318,15 +413,17 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   if (!want_logits) return PEARL_OK;
   const int first = logits_all ? 0 : M - 1;
   const int rows = M - first;
-  rmsnorm_kernel<<<rows, 256, 0, st>>>(m.h, m.final_norm, m.x, d, c.norm_eps, first);
-  PEARL_CUDA_TRY(cudaGetLastError());
-  count_launch();
+  rc = launch_pdl(rmsnorm_kernel, dim3(rows), dim3(256), 0, st, m.h, m.final_norm, m.x, d, c.norm_eps, first);
+  if (rc) return rc;
   EpiArgs s{};
   s.kind = EPI_STORE_F32;
   s.out_f32 = logits;
   s.ld = c.vocab;
   return launch_gemm(m, m.lm_head, m.x, rows, c.vocab, d, s, st);
 }
+
+std::once_flag g_attn_once;
+cudaError_t g_attn_err = cudaSuccess;
 
 }  // namespace
 }  // namespace pearl
@@ -340,8 +437,8 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   PEARL_ARG_CHECK(c.head_dim == 64 || c.head_dim == 128, "head_dim must be 64 or 128");
   PEARL_ARG_CHECK(c.n_heads % c.n_kv_heads == 0, "n_heads % n_kv_heads");
   PEARL_ARG_CHECK(c.d_model % 8 == 0 && c.ffn % 8 == 0, "d_model and ffn must be multiples of 8");
-  PEARL_ARG_CHECK(c.max_tokens >= 1 && c.max_tokens <= 256, "max_tokens in [1, 256]");
-  PEARL_ARG_CHECK(static_cast<size_t>(c.max_seq) * 4 <= 200 * 1024, "max_seq too large for attention smem");
+  PEARL_ARG_CHECK(c.max_tokens >= 1 && c.max_tokens <= 64, "max_tokens in [1, 64]");
+  PEARL_ARG_CHECK(c.max_seq >= 1, "max_seq >= 1");
   Llama* m = new Llama();
   m->cfg = c;
   m->embed = static_cast<const bf16*>(ptrs[0]);
@@ -359,6 +456,7 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   }
   const size_t T = static_cast<size_t>(c.max_tokens);
   const size_t wide = std::max<size_t>(std::max<size_t>(c.d_model, c.ffn), static_cast<size_t>(c.n_heads) * c.head_dim);
+  m->max_chunks = (c.max_seq + kAttnChunk - 1) / kAttnChunk;
   auto fail = [&](cudaError_t e) {
     set_error(std::string("pearl_llama_create: ") + cudaGetErrorString(e));
     delete m;
@@ -370,12 +468,14 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   if ((e = cudaMalloc(&m->q, T * c.n_heads * c.head_dim * sizeof(bf16)))) return fail(e);
   if ((e = cudaMalloc(&m->o, T * c.n_heads * c.head_dim * sizeof(bf16)))) return fail(e);
   if ((e = cudaMalloc(&m->act, T * c.ffn * sizeof(bf16)))) return fail(e);
-  const size_t attn_smem = static_cast<size_t>(c.max_seq) * sizeof(float);
-  if (attn_smem > 48 * 1024) {
-    if ((e = cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(attn_smem))))
-      return fail(e);
-  }
+  if ((e = cudaMalloc(&m->attn_part, T * c.n_heads * m->max_chunks * (c.head_dim + 2) * sizeof(float)))) return fail(e);
+  if ((e = cudaMalloc(&m->attn_flags, c.n_heads * sizeof(int)))) return fail(e);
+  if ((e = cudaMemset(m->attn_flags, 0, c.n_heads * sizeof(int)))) return fail(e);
+  std::call_once(g_attn_once, [] {
+    g_attn_err = cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(attention_smem_bytes(64, 128)));
+  });
+  if (g_attn_err) return fail(g_attn_err);
   if (c.gemm_kind == PEARL_GEMM_TCGEN05) {
     int rc = tc_init(m->tc, c);
     if (rc) {
@@ -395,6 +495,8 @@ extern "C" int pearl_llama_destroy(void* handle) {
   cudaFree(m->q);
   cudaFree(m->o);
   cudaFree(m->act);
+  cudaFree(m->attn_part);
+  cudaFree(m->attn_flags);
   tc_free(m->tc);
   delete m;
   return PEARL_OK;
@@ -413,14 +515,8 @@ extern "C" int pearl_gemm(int kind, const void* W, const void* X, float* Y, int 
   e.out_f32 = Y;
   e.ld = N;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (kind == PEARL_GEMM_CUDACORE) {
-    const int rows_per_block = kGemvWarps * kGemvRows;
-    gemv_kernel<<<(N + rows_per_block - 1) / rows_per_block, kGemvWarps * 32, 0, st>>>(
-        static_cast<const bf16*>(W), static_cast<const bf16*>(X), M, N, K, e);
-    PEARL_CUDA_TRY(cudaGetLastError());
-    count_launch();
-    return PEARL_OK;
-  }
+  if (kind == PEARL_GEMM_CUDACORE)
+    return launch_gemv(static_cast<const bf16*>(W), static_cast<const bf16*>(X), M, N, K, e, st);
   std::lock_guard<std::mutex> lk(g_gemm_mu);
   if (!g_gemm_ctx.partials) {
     pearl_llama_config c{};
@@ -466,9 +562,8 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
     if (rc) return rc;
   }
   if (flags & PEARL_FWD_ADVANCE) {
-    advance_kernel<<<1, 1, 0, st>>>(pos, n_tokens);
-    PEARL_CUDA_TRY(cudaGetLastError());
-    count_launch();
+    int rc = launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, pos, n_tokens);
+    if (rc) return rc;
   }
   return PEARL_OK;
 }
