@@ -44,6 +44,7 @@ constexpr int kMaxStages = 8;
 constexpr int kEBytes = kTileN * 64 * 4;       // epilogue staging [128][64] fp32
 constexpr int kTcThreads = 192;
 constexpr int kEpiThreads = 128;
+constexpr int kAccs = 4;  // TMEM accumulators (x 64 fp32 columns) in flight
 constexpr size_t kTcSmem = 1024 + kRingBytes + kEBytes + 512;
 
 struct TcArgs {
@@ -145,9 +146,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   float* E = reinterpret_cast<float*>(smem + kRingBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kEBytes);
   uint64_t* empty = full + kMaxStages;
-  uint64_t* acc_full = empty + kMaxStages;   // [2]
-  uint64_t* acc_empty = acc_full + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* acc_full = empty + kMaxStages;   // [kAccs]
+  uint64_t* acc_empty = acc_full + kAccs;    // [kAccs]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kAccs);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kAccs; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], kEpiThreads);
     }
@@ -171,8 +172,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
   }
   if (warp == 1) {
-    // two accumulators x 64 fp32 columns (up to 4 token tiles of 16)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+    // kAccs accumulators x 64 fp32 columns (up to 4 token tiles of 16)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -238,8 +239,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int ui = 0; ui < my_units; ++ui) {
         int t, sp, k0, k1;
         unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
-        const int b = ui & 1;
-        if (ui >= 2) mbar_wait(&acc_empty[b], ((ui >> 1) - 1) & 1);
+        const int b = ui % kAccs;
+        if (ui >= kAccs) mbar_wait(&acc_empty[b], ((ui / kAccs) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + b * 64;
         for (int kb = k0; kb < k1; ++kb, ++it) {
@@ -264,12 +265,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int lanegrp = warp & 3;  // TMEM lane quarter this warp may access
     const int row = lanegrp * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127
-    const int TOKP = NT * kTokTile;
     for (int ui = 0; ui < my_units; ++ui) {
       int tile, split, k0, k1;
       unit_range(a, blockIdx.x + ui * gridDim.x, tile, split, k0, k1);
-      const int b = ui & 1;
-      mbar_wait(&acc_full[b], (ui >> 1) & 1);
+      const int b = ui % kAccs;
+      mbar_wait(&acc_full[b], (ui / kAccs) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float v[kMaxTokTiles][16];
       for (int j = 0; j < NT; ++j)
@@ -281,22 +281,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int c = 0; c < 16; ++c) E[row * 64 + j * 16 + c] = v[j][c];
       } else {
-        float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * TOKP;
-        for (int j = 0; j < NT; ++j)
-#pragma unroll
-          for (int c = 0; c < 16; c += 4)
-            *reinterpret_cast<float4*>(dst + j * 16 + c) = make_float4(v[j][c], v[j][c + 1], v[j][c + 2], v[j][c + 3]);
-        __threadfence();
-        epi_bar();
-        if (et == 0) *s_last = (atomicAdd(&a.flags[tile], 1) == a.S - 1);
+        // compact fp32 partial [row][M] of this split
+        float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * a.M;
+        for (int t = 0; t < a.M; ++t) dst[t] = v[t >> 4][t & 15];
+        epi_bar();  // all partial stores of the CTA precede the releasing atomic
+        if (et == 0) {
+          int old;
+          asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.flags + tile) : "memory");
+          *s_last = (old == a.S - 1);
+        }
         epi_bar();
         if (!*s_last) continue;
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         // fixed split order => independent of arrival order and of M
         for (int t = 0; t < a.M; ++t) {
           float acc = 0.f;
           for (int s = 0; s < a.S; ++s)
-            acc += __ldcg(a.partials + ((static_cast<size_t>(tile) * a.S + s) * kTileN + row) * TOKP + t);
+            acc += __ldcg(a.partials + ((static_cast<size_t>(tile) * a.S + s) * kTileN + row) * a.M + t);
           E[row * 64 + t] = acc;
         }
         if (et == 0) a.flags[tile] = 0;
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
 // ---- host side ---------------------------------------------------------------

@@ -294,7 +294,12 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
     float m = -INFINITY;
     for (int j = 0; j < kAttnChunk; ++j) m = fmaxf(m, st[j]);
     float l = 0.f;
-    for (int j = 0; j < kAttnChunk; ++j) l += (st[j] == -INFINITY) ? 0.f : expf(st[j] - m);
+    float* pw = S + tt * kAttnChunk;  // overwrite scores with exp weights
+    for (int j = 0; j < kAttnChunk; ++j) {
+      const float p = (st[j] == -INFINITY) ? 0.f : expf(st[j] - m);
+      pw[j] = p;
+      l += p;
+    }
     stats[2 * tt] = m;
     stats[2 * tt + 1] = l;
   }
@@ -302,13 +307,10 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
   // exp-weighted V sum per (token, dim), sequential over the chunk
   for (int i = threadIdx.x; i < nt * hd; i += blockDim.x) {
     const int tt = i / hd, d = i % hd;
-    const float* st = S + tt * kAttnChunk;
+    const float* pw = S + tt * kAttnChunk;
     const float m = stats[2 * tt];
     float acc = 0.f;
-    for (int j = 0; j < nj; ++j) {
-      const float s = st[j];
-      if (s != -INFINITY) acc = fmaf(expf(s - m), __bfloat162float(Vs[j * hd + d]), acc);
-    }
+    for (int j = 0; j < nj; ++j) acc = fmaf(pw[j], __bfloat162float(Vs[j * hd + d]), acc);
     float* pr = a.part + ((static_cast<size_t>(t_first + tt) * a.H + h) * a.max_chunks + c) * (hd + 2);
     pr[2 + d] = acc;
     if (d == 0) {
@@ -316,13 +318,16 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
       pr[1] = stats[2 * tt + 1];
     }
   }
-  // last block of head h combines
-  __threadfence();
+  // last block of head h combines (release / acquire handoff through the counter)
   __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&a.flags[h], 1) == n_chunks - 1);
+  if (threadIdx.x == 0) {
+    int old;
+    asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.flags + h) : "memory");
+    s_last = (old == n_chunks - 1);
+  }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   for (int i = threadIdx.x; i < a.M * hd; i += blockDim.x) {
     const int t = i / hd, d = i % hd;
     const int nc = (p0 + t) / kAttnChunk + 1;  // chunks covering 0..p0+t
