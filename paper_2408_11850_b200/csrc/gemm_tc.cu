@@ -293,12 +293,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         epi_bar();
         if (!*s_last) continue;
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        // fixed split order => independent of arrival order and of M
-        for (int t = 0; t < a.M; ++t) {
+        // fixed split order => independent of arrival order and of M.
+        // (row, token) items over the 128 epilogue threads; all S partial
+        // loads of an item are issued before the in-order sum.
+        for (int idx = et; idx < kTileN * a.M; idx += kEpiThreads) {
+          const int r = idx / a.M, t = idx % a.M;
+          const float* src = a.partials + (static_cast<size_t>(tile) * a.S * kTileN + r) * a.M + t;
+          const size_t sstride = static_cast<size_t>(kTileN) * a.M;
+          float p[32];
+#pragma unroll
+          for (int s = 0; s < 32; ++s) p[s] = (s < a.S) ? __ldcg(src + s * sstride) : 0.f;
           float acc = 0.f;
-          for (int s = 0; s < a.S; ++s)
-            acc += __ldcg(a.partials + ((static_cast<size_t>(tile) * a.S + s) * kTileN + row) * a.M + t);
-          E[row * 64 + t] = acc;
+#pragma unroll
+          for (int s = 0; s < 32; ++s)
+            if (s < a.S) acc += p[s];
+          E[r * 64 + t] = acc;
         }
         if (et == 0) a.flags[tile] = 0;
       }

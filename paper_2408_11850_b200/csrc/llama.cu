@@ -104,15 +104,31 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const bf16* __r
 }
 
 // x[t] = bf16(h[t] * rsqrt(mean(h[t]^2) + eps) * g); one block per token,
-// fixed reduction order.
-__global__ void rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g, bf16* __restrict__ x,
-                               int d, float eps, int row_off) {
+// fixed reduction order.  The row is read once with all 16-byte loads in
+// flight (d <= 8192: at most 8 float4 per thread) and kept in registers.
+constexpr int kNormThreads = 256;
+constexpr int kNormVec = 8;
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g,
+                                                               bf16* __restrict__ x, int d, float eps, int row_off) {
   pdl_wait();
   pdl_trigger();
   const int t = blockIdx.x + row_off;
-  const float* hr = h + static_cast<size_t>(t) * d;
+  const float4* hr = reinterpret_cast<const float4*>(h + static_cast<size_t>(t) * d);
+  const int nv = d / 4;
+  float4 v[kNormVec];
+#pragma unroll
+  for (int i = 0; i < kNormVec; ++i) {
+    const int j = threadIdx.x + i * kNormThreads;
+    v[i] = j < nv ? hr[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(hr[i], hr[i], ss);
+#pragma unroll
+  for (int i = 0; i < kNormVec; ++i) {
+    ss = fmaf(v[i].x, v[i].x, ss);
+    ss = fmaf(v[i].y, v[i].y, ss);
+    ss = fmaf(v[i].z, v[i].z, ss);
+    ss = fmaf(v[i].w, v[i].w, ss);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   __shared__ float ws[32];
@@ -121,13 +137,23 @@ __global__ void rmsnorm_kernel(const float* __restrict__ h, const float* __restr
   __syncthreads();
   if (threadIdx.x == 0) {
     float tot = 0.f;
-    for (int w = 0; w < (blockDim.x >> 5); ++w) tot += ws[w];
+    for (int w = 0; w < kNormThreads / 32; ++w) tot += ws[w];
     s_rs = 1.0f / sqrtf(tot / static_cast<float>(d) + eps);
   }
   __syncthreads();
   const float rs = s_rs;
-  bf16* xr = x + static_cast<size_t>(blockIdx.x) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) xr[i] = __float2bfloat16(hr[i] * rs * g[i]);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  uint2* xr = reinterpret_cast<uint2*>(x + static_cast<size_t>(blockIdx.x) * d);
+#pragma unroll
+  for (int i = 0; i < kNormVec; ++i) {
+    const int j = threadIdx.x + i * kNormThreads;
+    if (j < nv) {
+      const float4 gg = g4[j];
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(v[i].x * rs * gg.x, v[i].y * rs * gg.y);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(v[i].z * rs * gg.z, v[i].w * rs * gg.w);
+      xr[j] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    }
+  }
 }
 
 __global__ void advance_kernel(int32_t* pos, int n) {
@@ -259,6 +285,7 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
   bf16* Vs = Ks + kAttnChunk * hd;                                // [64][hd]
   float* S = reinterpret_cast<float*>(Vs + kAttnChunk * hd);      // [nt][64]
   float* stats = S + nt * kAttnChunk;                             // [nt][2]
+  bf16* Qs = reinterpret_cast<bf16*>(stats + 2 * ((nt + 1) & ~1)); // [nt][hd], 16-byte aligned
   const size_t kstride = static_cast<size_t>(a.KV) * hd;
   // stage K / V rows (16-byte vectors)
   const int vec_per_row = hd / 8;
@@ -268,13 +295,18 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
     reinterpret_cast<uint4*>(Ks + j * hd)[v] = *reinterpret_cast<const uint4*>(a.kc + g);
     reinterpret_cast<uint4*>(Vs + j * hd)[v] = *reinterpret_cast<const uint4*>(a.vc + g);
   }
+  for (int i = threadIdx.x; i < nt * vec_per_row; i += blockDim.x) {
+    const int tt = i / vec_per_row, v = i % vec_per_row;
+    reinterpret_cast<uint4*>(Qs + tt * hd)[v] =
+        *reinterpret_cast<const uint4*>(a.q + (static_cast<size_t>(t_first + tt) * a.H + h) * hd + v * 8);
+  }
   __syncthreads();
   // scores: one thread per (token, position); fixed sequential dot over hd
   for (int i = threadIdx.x; i < nt * kAttnChunk; i += blockDim.x) {
     const int t = t_first + i / kAttnChunk, j = i % kAttnChunk;
     float s = -INFINITY;
     if (j < nj && j0 + j <= p0 + t) {
-      const bf16* qr = a.q + (static_cast<size_t>(t) * a.H + h) * hd;
+      const bf16* qr = Qs + (t - t_first) * hd;
       const bf16* kr = Ks + j * hd;
       float acc = 0.f;
       for (int d = 0; d < hd; d += 2) {
@@ -328,18 +360,38 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
   __syncthreads();
   if (!s_last) return;
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  constexpr int kB = 16;  // chunks per batch of in-flight loads
   for (int i = threadIdx.x; i < a.M * hd; i += blockDim.x) {
     const int t = i / hd, d = i % hd;
     const int nc = (p0 + t) / kAttnChunk + 1;  // chunks covering 0..p0+t
     const float* pt = a.part + (static_cast<size_t>(t) * a.H + h) * a.max_chunks * (hd + 2);
     float mx = -INFINITY;
-    for (int cc = 0; cc < nc; ++cc) mx = fmaxf(mx, __ldcg(pt + cc * (hd + 2)));
+    for (int c0 = 0; c0 < nc; c0 += kB) {
+      float mm[kB];
+#pragma unroll
+      for (int cc = 0; cc < kB; ++cc) mm[cc] = (c0 + cc < nc) ? __ldcg(pt + (c0 + cc) * (hd + 2)) : -INFINITY;
+#pragma unroll
+      for (int cc = 0; cc < kB; ++cc) mx = fmaxf(mx, mm[cc]);
+    }
     float L = 0.f, O = 0.f;
-    for (int cc = 0; cc < nc; ++cc) {
-      const float* pc = pt + cc * (hd + 2);
-      const float w = expf(__ldcg(pc) - mx);
-      L = fmaf(w, __ldcg(pc + 1), L);
-      O = fmaf(w, __ldcg(pc + 2 + d), O);
+    for (int c0 = 0; c0 < nc; c0 += kB) {
+      float mm[kB], ll[kB], oo[kB];
+#pragma unroll
+      for (int cc = 0; cc < kB; ++cc) {
+        const bool ok = c0 + cc < nc;
+        const float* pc = pt + (c0 + cc) * (hd + 2);
+        mm[cc] = ok ? __ldcg(pc) : 0.f;
+        ll[cc] = ok ? __ldcg(pc + 1) : 0.f;
+        oo[cc] = ok ? __ldcg(pc + 2 + d) : 0.f;
+      }
+#pragma unroll
+      for (int cc = 0; cc < kB; ++cc) {
+        if (c0 + cc < nc) {
+          const float w = expf(mm[cc] - mx);
+          L = fmaf(w, ll[cc], L);
+          O = fmaf(w, oo[cc], O);
+        }
+      }
     }
     a.o[(static_cast<size_t>(t) * a.H + h) * hd + d] = __float2bfloat16(O / L);
   }
@@ -348,7 +400,7 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
 
 size_t attention_smem_bytes(int T, int hd) {
   return static_cast<size_t>(2) * kAttnChunk * hd * sizeof(bf16) + static_cast<size_t>(T) * kAttnChunk * 4 +
-         static_cast<size_t>(T) * 2 * 4 + 16;
+         static_cast<size_t>(T + 1) * 2 * 4 + static_cast<size_t>(T) * hd * sizeof(bf16) + 64;
 }
 
 // ---------------------------------------------------------------------------
@@ -379,7 +431,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   const size_t attn_smem = attention_smem_bytes(M, hd);
   for (int l = 0; l < c.n_layers; ++l) {
     const LayerW& L = m.layers[l];
-    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
+    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
     if (rc) return rc;
     EpiArgs e{};
     e.kind = EPI_QKV;
@@ -404,7 +456,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     r.ld = d;
     rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
     if (rc) return rc;
-    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(256), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
+    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
     if (rc) return rc;
     EpiArgs g{};
     g.kind = EPI_SWIGLU;
@@ -418,7 +470,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   if (!want_logits) return PEARL_OK;
   const int first = logits_all ? 0 : M - 1;
   const int rows = M - first;
-  rc = launch_pdl(rmsnorm_kernel, dim3(rows), dim3(256), 0, st, m.h, m.final_norm, m.x, d, c.norm_eps, first);
+  rc = launch_pdl(rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, st, m.h, m.final_norm, m.x, d, c.norm_eps, first);
   if (rc) return rc;
   EpiArgs s{};
   s.kind = EPI_STORE_F32;
@@ -442,8 +494,9 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   PEARL_ARG_CHECK(c.head_dim == 64 || c.head_dim == 128, "head_dim must be 64 or 128");
   PEARL_ARG_CHECK(c.n_heads % c.n_kv_heads == 0, "n_heads % n_kv_heads");
   PEARL_ARG_CHECK(c.d_model % 8 == 0 && c.ffn % 8 == 0, "d_model and ffn must be multiples of 8");
+  PEARL_ARG_CHECK(c.d_model <= 4 * kNormThreads * kNormVec, "d_model too large for the norm kernel");
   PEARL_ARG_CHECK(c.max_tokens >= 1 && c.max_tokens <= 64, "max_tokens in [1, 64]");
-  PEARL_ARG_CHECK(c.max_seq >= 1, "max_seq >= 1");
+  PEARL_ARG_CHECK(c.max_seq >= 1 && c.max_seq <= 4096, "max_seq in [1, 4096]");
   Llama* m = new Llama();
   m->cfg = c;
   m->embed = static_cast<const bf16*>(ptrs[0]);

@@ -19,12 +19,26 @@ m = llama.LlamaModel(cfg, w, gemm=gemm, max_seq=512, max_tokens=64)
 toks = torch.full((M,), 5, dtype=torch.int32, device="cuda")
 pos = torch.tensor([192], dtype=torch.int32, device="cuda")
 out = torch.empty(M, cfg.vocab, device="cuda")
-for _ in range(iters):
-    m.forward(toks, M, pos, 0, out)
-torch.cuda.synchronize()
-s, e = torch.cuda.Event(True), torch.cuda.Event(True)
-s.record()
-for _ in range(5):
-    m.forward(toks, M, pos, 0, out)
-e.record(); e.synchronize()
-print(f"{name} M={M} {gemm}: {s.elapsed_time(e)/5:.3f} ms/forward, {cfg.weight_bytes()/(s.elapsed_time(e)/5e3)/1e9:.0f} GB/s weights")
+def timed(stream, graph=False):
+    with torch.cuda.stream(stream):
+        for _ in range(iters):
+            m.forward(toks, M, pos, 0, out, stream)
+        g = None
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                m.forward(toks, M, pos, 0, out)
+        stream.synchronize()
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        for _ in range(5):
+            if g is not None:
+                g.replay()
+            else:
+                m.forward(toks, M, pos, 0, out, stream)
+        e.record(); e.synchronize()
+        return s.elapsed_time(e) / 5
+for label, st, gr in (("default-stream", torch.cuda.default_stream(), False), ("side-stream", torch.cuda.Stream(), False),
+                      ("cuda-graph", torch.cuda.Stream(), True)):
+    t = timed(st, gr)
+    print(f"{name} M={M} {gemm} {label}: {t:.3f} ms/forward, {cfg.weight_bytes()/(t/1e3)/1e9:.0f} GB/s weights", flush=True)
