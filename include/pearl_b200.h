@@ -173,6 +173,12 @@ int pearl_llama_forward(void* handle, const int32_t* tokens, int n_tokens, int32
 
 size_t pearl_llama_workspace_bytes(void* handle, int n_tokens);
 
+/* Diagnostic: one eager forward with an event after every launch; out_ms
+ * (float[10]) receives device ms per op {embed, rmsnorm, qkv, attention, o,
+ * gate_up, down, lm_head, other} and the total. */
+int pearl_llama_profile(void* handle, const int32_t* tokens, int n_tokens, int32_t* pos, float* logits,
+                        float* out_ms, void* stream);
+
 /* Standalone contraction Y[M, N] (fp32) = X[M, K] (bf16) . W[N, K]^T (bf16)
  * on the given engine (PEARL_GEMM_*), for tests and microbenchmarks.
  * splits = 0 lets the planner pick the split-K factor (tcgen05 only). */

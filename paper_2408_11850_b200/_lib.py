@@ -59,6 +59,7 @@ SIGNATURES = {
     "pearl_llama_destroy": (_i32, [_vp]),
     "pearl_llama_forward": (_i32, [_vp, _vp, _i32, _vp, _i32, _vp, _vp]),
     "pearl_llama_workspace_bytes": (_sz, [_vp, _i32]),
+    "pearl_llama_profile": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp, _vp]),
     "pearl_gemm": (_i32, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
     "pearl_gemm_splits": (_i32, [_i32, _i32]),
     "pearl_kv_rollback": (_i32, [_vp, _vp, _i32, _vp]),

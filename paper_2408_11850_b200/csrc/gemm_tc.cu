@@ -265,25 +265,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int lanegrp = warp & 3;  // TMEM lane quarter this warp may access
     const int row = lanegrp * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127
+    const int Mp = (a.M + 3) & ~3;  // partial row stride (float4 aligned)
     for (int ui = 0; ui < my_units; ++ui) {
       int tile, split, k0, k1;
       unit_range(a, blockIdx.x + ui * gridDim.x, tile, split, k0, k1);
       const int b = ui % kAccs;
       mbar_wait(&acc_full[b], (ui / kAccs) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float v[kMaxTokTiles][16];
-      for (int j = 0; j < NT; ++j)
-        tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * 64 + j * kTokTile, v[j]);
+      float v[kMaxTokTiles * 16];
+#pragma unroll
+      for (int j = 0; j < kMaxTokTiles; ++j)
+        if (j < NT) tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * 64 + j * kTokTile, v + 16 * j);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&acc_empty[b]);  // the MMA warp may reuse this accumulator
       if (a.S == 1) {
-        for (int j = 0; j < NT; ++j)
 #pragma unroll
-          for (int c = 0; c < 16; ++c) E[row * 64 + j * 16 + c] = v[j][c];
+        for (int q = 0; q < kMaxTokTiles * 4; ++q)
+          if (q < NT * 4)
+            *reinterpret_cast<float4*>(E + row * 64 + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       } else {
-        // compact fp32 partial [row][M] of this split
-        float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * a.M;
-        for (int t = 0; t < a.M; ++t) dst[t] = v[t >> 4][t & 15];
+        // this split's fp32 partial row: Mp contiguous floats (float4 stores)
+        float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * Mp;
+#pragma unroll
+        for (int q = 0; q < kMaxTokTiles * 4; ++q)
+          if (4 * q < Mp)
+            *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         epi_bar();  // all partial stores of the CTA precede the releasing atomic
         if (et == 0) {
           int old;
@@ -293,21 +299,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         epi_bar();
         if (!*s_last) continue;
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        // fixed split order => independent of arrival order and of M.
-        // (row, token) items over the 128 epilogue threads; all S partial
-        // loads of an item are issued before the in-order sum.
-        for (int idx = et; idx < kTileN * a.M; idx += kEpiThreads) {
-          const int r = idx / a.M, t = idx % a.M;
-          const float* src = a.partials + (static_cast<size_t>(tile) * a.S * kTileN + r) * a.M + t;
-          const size_t sstride = static_cast<size_t>(kTileN) * a.M;
-          float p[32];
+        // Fixed split order => independent of arrival order and of M.  Each
+        // thread owns one row; per 4-token quad all S float4 loads are in
+        // flight together, then summed in split order.
+        const float* src = a.partials + (static_cast<size_t>(tile) * a.S * kTileN + row) * Mp;
+        const size_t sstride = static_cast<size_t>(kTileN) * Mp;
+        for (int q = 0; q < Mp / 4; ++q) {
+          float4 p[16];
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int s0 = 0; s0 < a.S; s0 += 16) {
 #pragma unroll
-          for (int s = 0; s < 32; ++s) p[s] = (s < a.S) ? __ldcg(src + s * sstride) : 0.f;
-          float acc = 0.f;
+            for (int s = 0; s < 16; ++s)
+              if (s0 + s < a.S) p[s] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + s) * sstride + 4 * q));
 #pragma unroll
-          for (int s = 0; s < 32; ++s)
-            if (s < a.S) acc += p[s];
-          E[r * 64 + t] = acc;
+            for (int s = 0; s < 16; ++s)
+              if (s0 + s < a.S) {
+                acc.x += p[s].x;
+                acc.y += p[s].y;
+                acc.z += p[s].z;
+                acc.w += p[s].w;
+              }
+          }
+          *reinterpret_cast<float4*>(E + row * 64 + 4 * q) = acc;
         }
         if (et == 0) a.flags[tile] = 0;
       }
@@ -422,7 +435,8 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   for (auto& s : shapes) {
     const int S = tc_splits(s[0], s[1], ctx.num_sms);
     const int tiles = (s[0] + kTileN - 1) / kTileN;
-    pf = std::max(pf, static_cast<size_t>(tiles) * S * kTileN * kMaxTokTiles * kTokTile);
+    const int Sa = std::max(S, ctx.min_plan_splits);
+    pf = std::max(pf, static_cast<size_t>(tiles) * Sa * kTileN * kMaxTokTiles * kTokTile);
     flags = std::max(flags, tiles);
   }
   ctx.partial_floats = pf;
@@ -472,7 +486,8 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.flags = ctx.tile_flags;
   const int tiles = (N + kTileN - 1) / kTileN;
   a.units = tiles * a.S;
-  if (static_cast<size_t>(tiles) * a.S * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats || tiles > ctx.n_flags) {
+  if (a.S > 32 || static_cast<size_t>(tiles) * a.S * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
+      tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");
     return PEARL_ERR_ARG;
   }

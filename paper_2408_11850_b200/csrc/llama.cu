@@ -69,6 +69,23 @@ struct Llama {
   TcGemmCtx tc;           // tcgen05 path state (split-K scratch, descriptors)
 };
 
+// Optional per-op timing of an eager forward (pearl_llama_profile): an event
+// is recorded after every launch; deltas are attributed to the op label.
+struct OpProfiler {
+  bool on = false;
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  cudaEvent_t start = nullptr;
+  void mark(int op, cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    marks.emplace_back(op, e);
+  }
+};
+OpProfiler g_prof;
+enum ProfOp { OP_EMBED = 0, OP_NORM, OP_QKV, OP_ATTN, OP_O, OP_GU, OP_DOWN, OP_HEAD, OP_OTHER, OP_COUNT };
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -426,6 +443,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   const int nq = H * hd, nkv = KV * hd;
   int rc = launch_pdl(embed_kernel, dim3(M), dim3(256), 0, st, tokens, m.embed, m.h, d, c.vocab);
   if (rc) return rc;
+  g_prof.mark(OP_EMBED, st);
   const size_t layer_kv = static_cast<size_t>(c.max_seq) * nkv;
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
   const size_t attn_smem = attention_smem_bytes(M, hd);
@@ -433,6 +451,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     const LayerW& L = m.layers[l];
     rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
     if (rc) return rc;
+    g_prof.mark(OP_NORM, st);
     EpiArgs e{};
     e.kind = EPI_QKV;
     e.out_bf16 = m.q;
@@ -447,36 +466,45 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     e.hd = hd;
     rc = launch_gemm(m, L.wqkv, m.x, M, nq + 2 * nkv, d, e, st);
     if (rc) return rc;
+    g_prof.mark(OP_QKV, st);
     AttnArgs aa{m.q, e.kc, e.vc, m.o, m.attn_part, m.attn_flags, pos, pos_add, M, H, KV, hd, m.max_chunks, scale};
     rc = launch_pdl(attention_kernel, dim3(H, m.max_chunks), dim3(128), attn_smem, st, aa);
     if (rc) return rc;
+    g_prof.mark(OP_ATTN, st);
     EpiArgs r{};
     r.kind = EPI_RESID;
     r.out_f32 = m.h;
     r.ld = d;
     rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
     if (rc) return rc;
+    g_prof.mark(OP_O, st);
     rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
     if (rc) return rc;
+    g_prof.mark(OP_NORM, st);
     EpiArgs g{};
     g.kind = EPI_SWIGLU;
     g.out_bf16 = m.act;
     g.ld = c.ffn;
     rc = launch_gemm(m, L.wgu, m.x, M, 2 * c.ffn, d, g, st);
     if (rc) return rc;
+    g_prof.mark(OP_GU, st);
     rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r, st);
     if (rc) return rc;
+    g_prof.mark(OP_DOWN, st);
   }
   if (!want_logits) return PEARL_OK;
   const int first = logits_all ? 0 : M - 1;
   const int rows = M - first;
   rc = launch_pdl(rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, st, m.h, m.final_norm, m.x, d, c.norm_eps, first);
   if (rc) return rc;
+  g_prof.mark(OP_NORM, st);
   EpiArgs s{};
   s.kind = EPI_STORE_F32;
   s.out_f32 = logits;
   s.ld = c.vocab;
-  return launch_gemm(m, m.lm_head, m.x, rows, c.vocab, d, s, st);
+  rc = launch_gemm(m, m.lm_head, m.x, rows, c.vocab, d, s, st);
+  g_prof.mark(OP_HEAD, st);
+  return rc;
 }
 
 std::once_flag g_attn_once;
@@ -586,6 +614,7 @@ extern "C" int pearl_gemm(int kind, const void* W, const void* X, float* Y, int 
     c.ffn = 28672;
     c.vocab = 131072;
     c.max_tokens = 64;
+    g_gemm_ctx.min_plan_splits = 16;
     int rc = tc_init(g_gemm_ctx, c);
     if (rc) return rc;
   }
@@ -624,4 +653,32 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
     if (rc) return rc;
   }
   return PEARL_OK;
+}
+
+// Per-op device time (ms) of one eager forward: out[op] for op in
+// {embed, norm, qkv, attn, o, gate_up, down, lm_head, other}; out[9] = total.
+extern "C" int pearl_llama_profile(void* handle, const int32_t* tokens, int n_tokens, int32_t* pos, float* logits,
+                                   float* out_ms, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PEARL_CUDA_TRY(cudaStreamSynchronize(st));
+  g_prof.on = true;
+  g_prof.marks.clear();
+  cudaEventCreate(&g_prof.start);
+  cudaEventRecord(g_prof.start, st);
+  int rc = pearl_llama_forward(handle, tokens, n_tokens, pos, 0, logits, stream);
+  g_prof.on = false;
+  PEARL_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i <= OP_COUNT; ++i) out_ms[i] = 0.f;
+  cudaEvent_t prev = g_prof.start;
+  for (auto& mk : g_prof.marks) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, prev, mk.second);
+    out_ms[mk.first] += ms;
+    out_ms[OP_COUNT] += ms;
+    prev = mk.second;
+  }
+  for (auto& mk : g_prof.marks) cudaEventDestroy(mk.second);
+  cudaEventDestroy(g_prof.start);
+  g_prof.marks.clear();
+  return rc;
 }

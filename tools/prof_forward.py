@@ -42,3 +42,12 @@ for label, st, gr in (("default-stream", torch.cuda.default_stream(), False), ("
                       ("cuda-graph", torch.cuda.Stream(), True)):
     t = timed(st, gr)
     print(f"{name} M={M} {gemm} {label}: {t:.3f} ms/forward, {cfg.weight_bytes()/(t/1e3)/1e9:.0f} GB/s weights", flush=True)
+
+import numpy as np, ctypes
+from paper_2408_11850_b200 import _lib
+names = ["embed", "norm", "qkv", "attn", "o", "gate_up", "down", "lm_head", "other", "TOTAL"]
+buf = (ctypes.c_float * 10)()
+for rep in range(3):
+    _lib.load().pearl_llama_profile(m.handle, toks.data_ptr(), M, pos.data_ptr(), out.data_ptr(), buf,
+                                    torch.cuda.current_stream().cuda_stream)
+print("per-op ms (events between launches):", {n: round(buf[i], 3) for i, n in enumerate(names)})
