@@ -1,5 +1,6 @@
 // Library identity and error reporting for the C ABI (include/pearl_b200.h).
 #include <atomic>
+#include <cstdlib>
 #include <string>
 
 #include "common.h"
@@ -8,6 +9,13 @@ namespace pearl {
 thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 static std::atomic<unsigned long long> g_launches{0};
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PEARL_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
 void count_launch(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed); }
 }  // namespace pearl
 

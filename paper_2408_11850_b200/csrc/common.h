@@ -14,6 +14,8 @@ void set_error(const std::string& msg);
 // Every kernel launch issued by the library bumps this counter (read with
 // pearl_launch_count); during graph capture it counts captured nodes.
 void count_launch(int n = 1);
+// Programmatic dependent launch on/off (env PEARL_PDL=0 disables; diagnostics).
+bool pdl_enabled();
 
 #define PEARL_CUDA_TRY(expr)                                                              \
   do {                                                                                    \

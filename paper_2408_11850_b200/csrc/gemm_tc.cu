@@ -500,7 +500,7 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel, it->second.map, xmap, a));
   count_launch();
   return PEARL_OK;

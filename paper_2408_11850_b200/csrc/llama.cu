@@ -100,7 +100,7 @@ int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
   count_launch();
   return PEARL_OK;
@@ -325,14 +325,20 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
     if (j < nj && j0 + j <= p0 + t) {
       const bf16* qr = Qs + (t - t_first) * hd;
       const bf16* kr = Ks + j * hd;
-      float acc = 0.f;
-      for (int d = 0; d < hd; d += 2) {
-        const __nv_bfloat162 q2 = *reinterpret_cast<const __nv_bfloat162*>(qr + d);
-        const __nv_bfloat162 k2 = *reinterpret_cast<const __nv_bfloat162*>(kr + d);
-        acc = fmaf(__low2float(q2), __low2float(k2), acc);
-        acc = fmaf(__high2float(q2), __high2float(k2), acc);
+      // four interleaved partial sums (fixed order, independent of the token count)
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int d = 0; d < hd; d += 8) {
+        const uint4 qv = *reinterpret_cast<const uint4*>(qr + d);
+        const uint4 kv = *reinterpret_cast<const uint4*>(kr + d);
+        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w}, kw[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[u] = fmaf(__uint_as_float(qw[u] << 16), __uint_as_float(kw[u] << 16), acc[u]);
+          acc[u] = fmaf(__uint_as_float(qw[u] & 0xffff0000u), __uint_as_float(kw[u] & 0xffff0000u), acc[u]);
+        }
       }
-      s = acc * a.scale;
+      s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * a.scale;
     }
     S[i] = s;
   }
@@ -358,8 +364,14 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
     const int tt = i / hd, d = i % hd;
     const float* pw = S + tt * kAttnChunk;
     const float m = stats[2 * tt];
-    float acc = 0.f;
-    for (int j = 0; j < nj; ++j) acc = fmaf(pw[j], __bfloat162float(Vs[j * hd + d]), acc);
+    float ac[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int j = 0; j < kAttnChunk; j += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j + u < nj) ac[u] = fmaf(pw[j + u], __bfloat162float(Vs[(j + u) * hd + d]), ac[u]);
+    }
+    const float acc = (ac[0] + ac[1]) + (ac[2] + ac[3]);
     float* pr = a.part + ((static_cast<size_t>(t_first + tt) * a.H + h) * a.max_chunks + c) * (hd + 2);
     pr[2 + d] = acc;
     if (d == 0) {
@@ -377,40 +389,65 @@ __global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
   __syncthreads();
   if (!s_last) return;
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  constexpr int kB = 16;  // chunks per batch of in-flight loads
-  for (int i = threadIdx.x; i < a.M * hd; i += blockDim.x) {
-    const int t = i / hd, d = i % hd;
-    const int nc = (p0 + t) / kAttnChunk + 1;  // chunks covering 0..p0+t
-    const float* pt = a.part + (static_cast<size_t>(t) * a.H + h) * a.max_chunks * (hd + 2);
-    float mx = -INFINITY;
-    for (int c0 = 0; c0 < nc; c0 += kB) {
-      float mm[kB];
+  // Every (token, dim) output sums its token's chunks in chunk order.  For
+  // contexts up to kFast chunks all loads of a thread's items are issued
+  // before any is used (one L2 round trip); longer contexts loop.
+  constexpr int kFast = 8;
+  const int per_thread = (a.M * hd + blockDim.x - 1) / blockDim.x;
+  if (n_chunks <= kFast && per_thread <= 4) {
+    float mm[4][kFast], ll[4][kFast], oo[4][kFast];
 #pragma unroll
-      for (int cc = 0; cc < kB; ++cc) mm[cc] = (c0 + cc < nc) ? __ldcg(pt + (c0 + cc) * (hd + 2)) : -INFINITY;
+    for (int k = 0; k < 4; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (k < per_thread && i < a.M * hd) {
+        const int t = i / hd, d = i % hd;
+        const int nc = (p0 + t) / kAttnChunk + 1;
+        const float* pt = a.part + (static_cast<size_t>(t) * a.H + h) * a.max_chunks * (hd + 2);
 #pragma unroll
-      for (int cc = 0; cc < kB; ++cc) mx = fmaxf(mx, mm[cc]);
-    }
-    float L = 0.f, O = 0.f;
-    for (int c0 = 0; c0 < nc; c0 += kB) {
-      float mm[kB], ll[kB], oo[kB];
-#pragma unroll
-      for (int cc = 0; cc < kB; ++cc) {
-        const bool ok = c0 + cc < nc;
-        const float* pc = pt + (c0 + cc) * (hd + 2);
-        mm[cc] = ok ? __ldcg(pc) : 0.f;
-        ll[cc] = ok ? __ldcg(pc + 1) : 0.f;
-        oo[cc] = ok ? __ldcg(pc + 2 + d) : 0.f;
-      }
-#pragma unroll
-      for (int cc = 0; cc < kB; ++cc) {
-        if (c0 + cc < nc) {
-          const float w = expf(mm[cc] - mx);
-          L = fmaf(w, ll[cc], L);
-          O = fmaf(w, oo[cc], O);
+        for (int cc = 0; cc < kFast; ++cc) {
+          const bool ok = cc < nc;
+          mm[k][cc] = ok ? __ldcg(pt + cc * (hd + 2)) : -INFINITY;
+          ll[k][cc] = ok ? __ldcg(pt + cc * (hd + 2) + 1) : 0.f;
+          oo[k][cc] = ok ? __ldcg(pt + cc * (hd + 2) + 2 + d) : 0.f;
         }
       }
     }
-    a.o[(static_cast<size_t>(t) * a.H + h) * hd + d] = __float2bfloat16(O / L);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (k < per_thread && i < a.M * hd) {
+        const int t = i / hd, d = i % hd;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int cc = 0; cc < kFast; ++cc) mx = fmaxf(mx, mm[k][cc]);
+        float L = 0.f, O = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < kFast; ++cc) {
+          if (mm[k][cc] != -INFINITY) {
+            const float w = expf(mm[k][cc] - mx);
+            L = fmaf(w, ll[k][cc], L);
+            O = fmaf(w, oo[k][cc], O);
+          }
+        }
+        a.o[(static_cast<size_t>(t) * a.H + h) * hd + d] = __float2bfloat16(O / L);
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < a.M * hd; i += blockDim.x) {
+      const int t = i / hd, d = i % hd;
+      const int nc = (p0 + t) / kAttnChunk + 1;
+      const float* pt = a.part + (static_cast<size_t>(t) * a.H + h) * a.max_chunks * (hd + 2);
+      float mx = -INFINITY;
+      for (int cc = 0; cc < nc; ++cc) mx = fmaxf(mx, __ldcg(pt + cc * (hd + 2)));
+      float L = 0.f, O = 0.f;
+      for (int cc = 0; cc < nc; ++cc) {
+        const float* pc = pt + cc * (hd + 2);
+        const float w = expf(__ldcg(pc) - mx);
+        L = fmaf(w, __ldcg(pc + 1), L);
+        O = fmaf(w, __ldcg(pc + 2 + d), O);
+      }
+      a.o[(static_cast<size_t>(t) * a.H + h) * hd + d] = __float2bfloat16(O / L);
+    }
   }
   if (threadIdx.x == 0) a.flags[h] = 0;
 }
