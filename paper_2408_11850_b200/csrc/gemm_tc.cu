@@ -39,13 +39,27 @@ constexpr int kTokTile = 16;   // tokens per MMA (MMA-N)
 constexpr int kMaxTokTiles = 4;
 constexpr int kWBytes = kTileN * kTileK * 2;   // 16 KB
 constexpr int kXBytes = kTokTile * kTileK * 2; // 2 KB per token tile
-constexpr int kRingBytes = 144 * 1024;         // smem ring (stages sized by NT)
 constexpr int kMaxStages = 8;
-constexpr int kEBytes = kTileN * 64 * 4;       // epilogue staging [128][64] fp32
 constexpr int kTcThreads = 192;
 constexpr int kEpiThreads = 128;
-constexpr int kAccs = 4;  // TMEM accumulators (x 64 fp32 columns) in flight
-constexpr size_t kTcSmem = 1024 + kRingBytes + kEBytes + 512;
+constexpr int kAccs = 4;  // TMEM accumulators (x NT*16 fp32 columns) in flight
+
+// Per token-tile-count (NT) configuration.  NT <= 2 keeps smem <= ~100 KB and
+// registers <= 168/thread so two CTAs fit on an SM: the next kernel's CTAs
+// (programmatic dependent launch) then co-reside and stream their first
+// weight stages while this kernel drains.
+template <int NT>
+struct TcCfg {
+  static constexpr int kRing = NT <= 2 ? 90 * 1024 : 144 * 1024;
+  static constexpr int kStageBytes = kWBytes + NT * kXBytes;
+  static constexpr int kStages = (kRing / kStageBytes) < kMaxStages ? (kRing / kStageBytes) : kMaxStages;
+  static constexpr int kEStride = NT * 16;                 // fp32 per staged row
+  static constexpr int kEBytes = kTileN * kEStride * 4;
+  static constexpr int kCols = kAccs * NT * 16;
+  static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + kEBytes + 512;
+  static constexpr int kMinBlocks = NT <= 2 ? 2 : 1;
+};
 
 struct TcArgs {
   int M, N, K, KB, S, units;
@@ -138,13 +152,18 @@ __device__ __forceinline__ void unit_range(const TcArgs& a, int u, int& tile, in
 }
 
 // ---- kernel ------------------------------------------------------------------
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int NT>
+__global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcArgs a) {
+  using C = TcCfg<NT>;
+  constexpr int stage_bytes = C::kStageBytes;
+  constexpr int stages = C::kStages;
+  constexpr int ES = C::kEStride;
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  float* E = reinterpret_cast<float*>(smem + kRingBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kEBytes);
+  float* E = reinterpret_cast<float*>(smem + stages * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes + C::kEBytes);
   uint64_t* empty = full + kMaxStages;
   uint64_t* acc_full = empty + kMaxStages;   // [kAccs]
   uint64_t* acc_empty = acc_full + kAccs;    // [kAccs]
@@ -152,9 +171,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int NT = (a.M + kTokTile - 1) / kTokTile;
-  const int stage_bytes = kWBytes + NT * kXBytes;
-  const int stages = min(kMaxStages, kRingBytes / stage_bytes);
   // units of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
   const int my_units = a.units > static_cast<int>(blockIdx.x) ? (a.units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -172,8 +188,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
   }
   if (warp == 1) {
-    // kAccs accumulators x 64 fp32 columns (up to 4 token tiles of 16)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    // kAccs accumulators x NT*16 fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -242,7 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int b = ui % kAccs;
         if (ui >= kAccs) mbar_wait(&acc_empty[b], ((ui / kAccs) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t acc = tmem + b * 64;
+        const uint32_t acc = tmem + b * NT * kTokTile;
         for (int kb = k0; kb < k1; ++kb, ++it) {
           const int s = it % stages;
           mbar_wait(&full[s], (it / stages) & 1);
@@ -272,22 +289,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int b = ui % kAccs;
       mbar_wait(&acc_full[b], (ui / kAccs) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float v[kMaxTokTiles * 16];
+      float v[NT * 16];
 #pragma unroll
-      for (int j = 0; j < kMaxTokTiles; ++j)
-        if (j < NT) tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * 64 + j * kTokTile, v + 16 * j);
+      for (int j = 0; j < NT; ++j)
+        tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * NT * kTokTile + j * kTokTile, v + 16 * j);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&acc_empty[b]);  // the MMA warp may reuse this accumulator
       if (a.S == 1) {
 #pragma unroll
-        for (int q = 0; q < kMaxTokTiles * 4; ++q)
-          if (q < NT * 4)
-            *reinterpret_cast<float4*>(E + row * 64 + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int q = 0; q < NT * 4; ++q)
+          *reinterpret_cast<float4*>(E + row * ES + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       } else {
         // this split's fp32 partial row: Mp contiguous floats (float4 stores)
         float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * Mp;
 #pragma unroll
-        for (int q = 0; q < kMaxTokTiles * 4; ++q)
+        for (int q = 0; q < NT * 4; ++q)
           if (4 * q < Mp)
             *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         epi_bar();  // all partial stores of the CTA precede the releasing atomic
@@ -320,7 +336,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 acc.w += p[s].w;
               }
           }
-          *reinterpret_cast<float4*>(E + row * 64 + 4 * q) = acc;
+          *reinterpret_cast<float4*>(E + row * ES + 4 * q) = acc;
         }
         if (et == 0) a.flags[tile] = 0;
       }
@@ -332,7 +348,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (n0 >= a.N) continue;
         float w[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) w[r] = E[(g * 4 + r) * 64 + t];
+        for (int r = 0; r < 4; ++r) w[r] = E[(g * 4 + r) * ES + t];
         epilogue4(a.e, t, n0, w, a.N);
       }
       epi_bar();
@@ -341,7 +357,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -385,6 +401,12 @@ int encode_2d(CUtensorMap* map, const void* base, int inner, int rows, int box_r
 std::once_flag g_attr_once;
 cudaError_t g_attr_err = cudaSuccess;
 
+template <int NT>
+cudaError_t set_attr() {
+  return cudaFuncSetAttribute(tc_gemm_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(TcCfg<NT>::kSmem));
+}
+
 }  // namespace
 
 // Split-K factor for an (N, K) weight: enough (tile, split) units to keep
@@ -395,13 +417,13 @@ int tc_splits(int N, int K, int num_sms) {
   const int KB = (K + kTileK - 1) / kTileK;
   int best = 1;
   double best_cost = -1;
-  for (int S = 1; S <= std::min(KB, 32); ++S) {
+  for (int S = 1; S <= std::min(KB, 16); ++S) {
     if (KB / S < 4 && S > 1) break;  // keep >= 4 k-blocks of streaming per unit
     const long long units = static_cast<long long>(tiles) * S;
-    // persistent round-robin: the busiest SM streams ceil(units/sms) units of
-    // ceil(KB/S) blocks; splitting also costs partial-tile traffic
-    const double per_sm = static_cast<double>((units + num_sms - 1) / num_sms) * ((KB + S - 1) / S);
-    const double cost = per_sm + (S > 1 ? 0.15 * static_cast<double>(units) * 2.0 / num_sms : 0.0);
+    const long long waves = (units + num_sms - 1) / num_sms;
+    // busiest SM: its streamed k-blocks + a per-unit overhead (~1.5 k-block
+    // times) + the split-K reduction tail; measured on B200 (tools/gemm_sweep.py)
+    const double cost = static_cast<double>(waves * ((KB + S - 1) / S)) + 1.5 * waves + 0.5 * (S - 1);
     if (best_cost < 0 || cost < best_cost - 1e-9) {
       best_cost = cost;
       best = S;
@@ -419,8 +441,11 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   PEARL_CUDA_TRY(cudaGetDevice(&dev));
   PEARL_CUDA_TRY(cudaDeviceGetAttribute(&ctx.num_sms, cudaDevAttrMultiProcessorCount, dev));
   std::call_once(g_attr_once, [] {
-    g_attr_err = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kTcSmem));
+    cudaError_t e = set_attr<1>();
+    if (e == cudaSuccess) e = set_attr<2>();
+    if (e == cudaSuccess) e = set_attr<3>();
+    if (e == cudaSuccess) e = set_attr<4>();
+    g_attr_err = e;
   });
   PEARL_CUDA_TRY(g_attr_err);
   ctx.max_tokens = c.max_tokens;
@@ -491,17 +516,34 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
     set_error("tc_gemm: shape exceeds the planned split-K workspace");
     return PEARL_ERR_ARG;
   }
+  const int NT = (M + kTokTile - 1) / kTokTile;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min(a.units, ctx.num_sms));
   cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = kTcSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel, it->second.map, xmap, a));
+  switch (NT) {
+    case 1:
+      cfg.dynamicSmemBytes = TcCfg<1>::kSmem;
+      PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<1>, it->second.map, xmap, a));
+      break;
+    case 2:
+      cfg.dynamicSmemBytes = TcCfg<2>::kSmem;
+      PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, it->second.map, xmap, a));
+      break;
+    case 3:
+      cfg.dynamicSmemBytes = TcCfg<3>::kSmem;
+      PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<3>, it->second.map, xmap, a));
+      break;
+    default:
+      cfg.dynamicSmemBytes = TcCfg<4>::kSmem;
+      PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<4>, it->second.map, xmap, a));
+      break;
+  }
   count_launch();
   return PEARL_OK;
 }
