@@ -45,7 +45,6 @@ struct LayerW {
   const bf16* wdown;
 };
 
-constexpr int kAttnChunk = 64;  // positions per attention work item
 
 struct Llama {
   pearl_llama_config cfg;
@@ -63,9 +62,6 @@ struct Llama {
   bf16* q = nullptr;      // [T, H hd]
   bf16* o = nullptr;      // [T, H hd]
   bf16* act = nullptr;    // [T, ffn]
-  float* attn_part = nullptr;  // [T, H, chunks, hd + 2] partial (m, l, o)
-  int* attn_flags = nullptr;   // [H] arrival counters (self-resetting)
-  int max_chunks = 0;
   TcGemmCtx tc;           // tcgen05 path state (split-K scratch, descriptors)
 };
 
@@ -261,200 +257,148 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
 
 // ---------------------------------------------------------------------------
 // K4: causal attention of the window's M queries over the KV cache.
-// Work item = (query head h, 64-position chunk c).  A block stages the
-// chunk's K and V rows of h's KV head in shared memory and, for every window
-// token t whose causal range reaches the chunk, computes fixed-order dot
-// products, the chunk's max / sum-of-exp and the exp-weighted V sum.  The
-// last block to finish head h combines the chunks of each token in chunk
-// order.  Each token's result therefore depends only on its own position and
-// the cache contents (batch invariance).
+// One block per (query head h, group of <= 16 window tokens); its 8 warps take 32-position chunks of the
+// context round-robin (chunk c -> warp c % 8).  Within a warp lane j owns
+// position c*32+j: it computes the full fixed-order q.k dot product for every
+// window token, the warp reduces max / sum-of-exp with shuffles, and the
+// exp-weighted V sum is accumulated with lanes over head dims.  Each warp
+// keeps a running (max, sum, o) per token over its chunks (online softmax in
+// chunk order); the block then merges the 8 warps' states in warp order.
+// Every step depends only on the token's own position and the cache, never
+// on how many tokens share the launch (batch invariance), and there is no
+// inter-block communication.
 // ---------------------------------------------------------------------------
+constexpr int kAttnWarps = 8;
+constexpr int kAttnLanesPos = 32;  // positions per warp chunk
+constexpr int kAttnTokens = 16;    // window tokens per block (grid.y = ceil(M / 16))
+
 struct AttnArgs {
   const bf16* q;      // [M, H, hd]
   const bf16* kc;     // layer cache [max_seq, KV, hd]
   const bf16* vc;
   bf16* o;            // [M, H, hd]
-  float* part;        // [T, H, chunks, hd + 2]
-  int* flags;         // [H]
   const int32_t* pos;
-  int pos_add, M, H, KV, hd, max_chunks;
+  int pos_add, M, H, KV, hd;
   float scale;
 };
 
-__global__ void __launch_bounds__(128) attention_kernel(AttnArgs a) {
+template <int HD>
+__global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(AttnArgs a) {
+  constexpr int PER = HD / 32;  // dims per lane (2 or 4)
   extern __shared__ __align__(16) unsigned char attn_smem[];
-  __shared__ int s_last;
   pdl_wait();
   pdl_trigger();
-  const int h = blockIdx.x, c = blockIdx.y;
-  const int hd = a.hd;
-  const int p0 = *a.pos + a.pos_add;          // position of window token 0
-  const int ctx_max = p0 + a.M;               // positions 0 .. ctx_max-1 exist
-  const int n_chunks = (ctx_max + kAttnChunk - 1) / kAttnChunk;
-  if (c >= n_chunks) return;                  // not part of this launch's work
+  const int h = blockIdx.x;
+  const int t0 = blockIdx.y * kAttnTokens;            // first window token of this block
+  const int MT = min(kAttnTokens, a.M - t0);          // tokens handled here
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p0 = *a.pos + a.pos_add + t0;             // position of the block's first token
+  const int ctx_max = p0 + MT;
+  const int n_chunks = (ctx_max + kAttnLanesPos - 1) / kAttnLanesPos;
   const int kvh = h / (a.H / a.KV);
-  const int j0 = c * kAttnChunk;
-  const int nj = min(kAttnChunk, ctx_max - j0);
-  // tokens whose causal range reaches this chunk: pos_t = p0 + t >= j0
-  const int t_first = max(0, j0 - p0);
-  const int nt = a.M - t_first;
-  bf16* Ks = reinterpret_cast<bf16*>(attn_smem);                 // [64][hd]
-  bf16* Vs = Ks + kAttnChunk * hd;                                // [64][hd]
-  float* S = reinterpret_cast<float*>(Vs + kAttnChunk * hd);      // [nt][64]
-  float* stats = S + nt * kAttnChunk;                             // [nt][2]
-  bf16* Qs = reinterpret_cast<bf16*>(stats + 2 * ((nt + 1) & ~1)); // [nt][hd], 16-byte aligned
-  const size_t kstride = static_cast<size_t>(a.KV) * hd;
-  // stage K / V rows (16-byte vectors)
-  const int vec_per_row = hd / 8;
-  for (int i = threadIdx.x; i < nj * vec_per_row; i += blockDim.x) {
-    const int j = i / vec_per_row, v = i % vec_per_row;
-    const size_t g = (j0 + j) * kstride + kvh * hd + v * 8;
-    reinterpret_cast<uint4*>(Ks + j * hd)[v] = *reinterpret_cast<const uint4*>(a.kc + g);
-    reinterpret_cast<uint4*>(Vs + j * hd)[v] = *reinterpret_cast<const uint4*>(a.vc + g);
+  const size_t kstride = static_cast<size_t>(a.KV) * HD;
+  // per-warp state [M][HD + 2] in smem: o (HD), m, l
+  float* st_all = reinterpret_cast<float*>(attn_smem);
+  float* st = st_all + static_cast<size_t>(warp) * MT * (HD + 2);
+  bf16* Qs = reinterpret_cast<bf16*>(st_all + static_cast<size_t>(kAttnWarps) * kAttnTokens * (HD + 2));  // [MT][HD]
+  for (int i = threadIdx.x; i < MT * HD / 8; i += blockDim.x) {
+    const int t = i / (HD / 8), v = i % (HD / 8);
+    reinterpret_cast<uint4*>(Qs + t * HD)[v] =
+        *reinterpret_cast<const uint4*>(a.q + (static_cast<size_t>(t0 + t) * a.H + h) * HD + v * 8);
   }
-  for (int i = threadIdx.x; i < nt * vec_per_row; i += blockDim.x) {
-    const int tt = i / vec_per_row, v = i % vec_per_row;
-    reinterpret_cast<uint4*>(Qs + tt * hd)[v] =
-        *reinterpret_cast<const uint4*>(a.q + (static_cast<size_t>(t_first + tt) * a.H + h) * hd + v * 8);
-  }
+  for (int i = lane; i < MT * (HD + 2); i += 32) st[i] = (i % (HD + 2) == HD) ? -INFINITY : 0.f;
   __syncthreads();
-  // scores: one thread per (token, position); fixed sequential dot over hd
-  for (int i = threadIdx.x; i < nt * kAttnChunk; i += blockDim.x) {
-    const int t = t_first + i / kAttnChunk, j = i % kAttnChunk;
-    float s = -INFINITY;
-    if (j < nj && j0 + j <= p0 + t) {
-      const bf16* qr = Qs + (t - t_first) * hd;
-      const bf16* kr = Ks + j * hd;
-      // four interleaved partial sums (fixed order, independent of the token count)
+  for (int c = warp; c < n_chunks; c += kAttnWarps) {
+    const int j = c * kAttnLanesPos + lane;  // this lane's position
+    const bool have = j < ctx_max;
+    // K row of position j into registers (16-byte loads, all in flight)
+    uint4 kr[HD / 8];
+#pragma unroll
+    for (int v = 0; v < HD / 8; ++v)
+      kr[v] = have ? *reinterpret_cast<const uint4*>(a.kc + j * kstride + kvh * HD + v * 8) : make_uint4(0, 0, 0, 0);
+    // V slice (PER dims of every position of the chunk) is read per step below
+    for (int t = 0; t < MT; ++t) {
+      const int pt = p0 + t;
+      if (c * kAttnLanesPos > pt) continue;  // chunk lies beyond this token's causal range
+      const bf16* qr = Qs + t * HD;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-      for (int d = 0; d < hd; d += 8) {
-        const uint4 qv = *reinterpret_cast<const uint4*>(qr + d);
-        const uint4 kv = *reinterpret_cast<const uint4*>(kr + d);
-        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w}, kw[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+      for (int v = 0; v < HD / 8; ++v) {
+        const uint4 qv = *reinterpret_cast<const uint4*>(qr + v * 8);
+        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w}, kw[4] = {kr[v].x, kr[v].y, kr[v].z, kr[v].w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           acc[u] = fmaf(__uint_as_float(qw[u] << 16), __uint_as_float(kw[u] << 16), acc[u]);
           acc[u] = fmaf(__uint_as_float(qw[u] & 0xffff0000u), __uint_as_float(kw[u] & 0xffff0000u), acc[u]);
         }
       }
-      s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * a.scale;
-    }
-    S[i] = s;
-  }
-  __syncthreads();
-  // per-token chunk max and sum of exp (sequential over the chunk)
-  for (int tt = threadIdx.x; tt < nt; tt += blockDim.x) {
-    const float* st = S + tt * kAttnChunk;
-    float m = -INFINITY;
-    for (int j = 0; j < kAttnChunk; ++j) m = fmaxf(m, st[j]);
-    float l = 0.f;
-    float* pw = S + tt * kAttnChunk;  // overwrite scores with exp weights
-    for (int j = 0; j < kAttnChunk; ++j) {
-      const float p = (st[j] == -INFINITY) ? 0.f : expf(st[j] - m);
-      pw[j] = p;
-      l += p;
-    }
-    stats[2 * tt] = m;
-    stats[2 * tt + 1] = l;
-  }
-  __syncthreads();
-  // exp-weighted V sum per (token, dim), sequential over the chunk
-  for (int i = threadIdx.x; i < nt * hd; i += blockDim.x) {
-    const int tt = i / hd, d = i % hd;
-    const float* pw = S + tt * kAttnChunk;
-    const float m = stats[2 * tt];
-    float ac[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-    for (int j = 0; j < kAttnChunk; j += 4) {
+      const bool valid = have && j <= pt;
+      const float s = valid ? ((acc[0] + acc[1]) + (acc[2] + acc[3])) * a.scale : -INFINITY;
+      // chunk max (fixed xor tree)
+      float cm = s;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j + u < nj) ac[u] = fmaf(pw[j + u], __bfloat162float(Vs[(j + u) * hd + d]), ac[u]);
-    }
-    const float acc = (ac[0] + ac[1]) + (ac[2] + ac[3]);
-    float* pr = a.part + ((static_cast<size_t>(t_first + tt) * a.H + h) * a.max_chunks + c) * (hd + 2);
-    pr[2 + d] = acc;
-    if (d == 0) {
-      pr[0] = m;
-      pr[1] = stats[2 * tt + 1];
-    }
-  }
-  // last block of head h combines (release / acquire handoff through the counter)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int old;
-    asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.flags + h) : "memory");
-    s_last = (old == n_chunks - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  // Every (token, dim) output sums its token's chunks in chunk order.  For
-  // contexts up to kFast chunks all loads of a thread's items are issued
-  // before any is used (one L2 round trip); longer contexts loop.
-  constexpr int kFast = 8;
-  const int per_thread = (a.M * hd + blockDim.x - 1) / blockDim.x;
-  if (n_chunks <= kFast && per_thread <= 4) {
-    float mm[4][kFast], ll[4][kFast], oo[4][kFast];
+      for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+      float* sr = st + t * (HD + 2);
+      const float m_old = sr[HD];
+      const float m_new = fmaxf(m_old, cm);
+      const float p = valid ? expf(s - m_new) : 0.f;
+      float ps = p;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = threadIdx.x + k * blockDim.x;
-      if (k < per_thread && i < a.M * hd) {
-        const int t = i / hd, d = i % hd;
-        const int nc = (p0 + t) / kAttnChunk + 1;
-        const float* pt = a.part + (static_cast<size_t>(t) * a.H + h) * a.max_chunks * (hd + 2);
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      const float corr = (m_old == -INFINITY) ? 0.f : expf(m_old - m_new);
+      // o[d] = corr * o[d] + sum_j p_j v_j[d], lanes over dims, positions in order
+      float ov[PER];
 #pragma unroll
-        for (int cc = 0; cc < kFast; ++cc) {
-          const bool ok = cc < nc;
-          mm[k][cc] = ok ? __ldcg(pt + cc * (hd + 2)) : -INFINITY;
-          ll[k][cc] = ok ? __ldcg(pt + cc * (hd + 2) + 1) : 0.f;
-          oo[k][cc] = ok ? __ldcg(pt + cc * (hd + 2) + 2 + d) : 0.f;
+      for (int e = 0; e < PER; ++e) ov[e] = 0.f;
+      const int jn = min(kAttnLanesPos, pt + 1 - c * kAttnLanesPos);
+      for (int jj = 0; jj < jn; ++jj) {
+        const float pj = __shfl_sync(0xffffffffu, p, jj);
+        const bf16* vr = a.vc + (c * kAttnLanesPos + jj) * kstride + kvh * HD + lane * PER;
+        if (PER == 4) {
+          const uint2 vv = *reinterpret_cast<const uint2*>(vr);
+          ov[0] = fmaf(pj, __uint_as_float(vv.x << 16), ov[0]);
+          ov[1] = fmaf(pj, __uint_as_float(vv.x & 0xffff0000u), ov[1]);
+          ov[2 % PER] = fmaf(pj, __uint_as_float(vv.y << 16), ov[2 % PER]);
+          ov[3 % PER] = fmaf(pj, __uint_as_float(vv.y & 0xffff0000u), ov[3 % PER]);
+        } else {
+          const uint32_t vv = *reinterpret_cast<const uint32_t*>(vr);
+          ov[0] = fmaf(pj, __uint_as_float(vv << 16), ov[0]);
+          ov[1 % PER] = fmaf(pj, __uint_as_float(vv & 0xffff0000u), ov[1 % PER]);
         }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = threadIdx.x + k * blockDim.x;
-      if (k < per_thread && i < a.M * hd) {
-        const int t = i / hd, d = i % hd;
-        float mx = -INFINITY;
-#pragma unroll
-        for (int cc = 0; cc < kFast; ++cc) mx = fmaxf(mx, mm[k][cc]);
-        float L = 0.f, O = 0.f;
-#pragma unroll
-        for (int cc = 0; cc < kFast; ++cc) {
-          if (mm[k][cc] != -INFINITY) {
-            const float w = expf(mm[k][cc] - mx);
-            L = fmaf(w, ll[k][cc], L);
-            O = fmaf(w, oo[k][cc], O);
-          }
-        }
-        a.o[(static_cast<size_t>(t) * a.H + h) * hd + d] = __float2bfloat16(O / L);
+      for (int e = 0; e < PER; ++e) sr[lane * PER + e] = fmaf(corr, sr[lane * PER + e], ov[e]);
+      __syncwarp();
+      if (lane == 0) {
+        sr[HD] = m_new;
+        sr[HD + 1] = fmaf(corr, sr[HD + 1], ps);
       }
-    }
-  } else {
-    for (int i = threadIdx.x; i < a.M * hd; i += blockDim.x) {
-      const int t = i / hd, d = i % hd;
-      const int nc = (p0 + t) / kAttnChunk + 1;
-      const float* pt = a.part + (static_cast<size_t>(t) * a.H + h) * a.max_chunks * (hd + 2);
-      float mx = -INFINITY;
-      for (int cc = 0; cc < nc; ++cc) mx = fmaxf(mx, __ldcg(pt + cc * (hd + 2)));
-      float L = 0.f, O = 0.f;
-      for (int cc = 0; cc < nc; ++cc) {
-        const float* pc = pt + cc * (hd + 2);
-        const float w = expf(__ldcg(pc) - mx);
-        L = fmaf(w, __ldcg(pc + 1), L);
-        O = fmaf(w, __ldcg(pc + 2 + d), O);
-      }
-      a.o[(static_cast<size_t>(t) * a.H + h) * hd + d] = __float2bfloat16(O / L);
+      __syncwarp();
     }
   }
-  if (threadIdx.x == 0) a.flags[h] = 0;
+  __syncthreads();
+  // merge the warps' states in warp order
+  for (int i = threadIdx.x; i < MT * HD; i += blockDim.x) {
+    const int t = i / HD, d = i % HD;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) mx = fmaxf(mx, st_all[(static_cast<size_t>(w) * MT + t) * (HD + 2) + HD]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) {
+      const float* sr = st_all + (static_cast<size_t>(w) * MT + t) * (HD + 2);
+      if (sr[HD] != -INFINITY) {
+        const float wt = expf(sr[HD] - mx);
+        L = fmaf(wt, sr[HD + 1], L);
+        O = fmaf(wt, sr[d], O);
+      }
+    }
+    a.o[(static_cast<size_t>(t0 + t) * a.H + h) * HD + d] = __float2bfloat16(O / L);
+  }
 }
 
-size_t attention_smem_bytes(int T, int hd) {
-  return static_cast<size_t>(2) * kAttnChunk * hd * sizeof(bf16) + static_cast<size_t>(T) * kAttnChunk * 4 +
-         static_cast<size_t>(T + 1) * 2 * 4 + static_cast<size_t>(T) * hd * sizeof(bf16) + 64;
+size_t attention_smem_bytes(int, int hd) {
+  return static_cast<size_t>(kAttnWarps) * kAttnTokens * (hd + 2) * 4 + static_cast<size_t>(kAttnTokens) * hd * 2 + 64;
 }
 
 // ---------------------------------------------------------------------------
@@ -504,8 +448,13 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     rc = launch_gemm(m, L.wqkv, m.x, M, nq + 2 * nkv, d, e, st);
     if (rc) return rc;
     g_prof.mark(OP_QKV, st);
-    AttnArgs aa{m.q, e.kc, e.vc, m.o, m.attn_part, m.attn_flags, pos, pos_add, M, H, KV, hd, m.max_chunks, scale};
-    rc = launch_pdl(attention_kernel, dim3(H, m.max_chunks), dim3(128), attn_smem, st, aa);
+    AttnArgs aa{m.q, e.kc, e.vc, m.o, pos, pos_add, M, H, KV, hd, scale};
+    if (hd == 128)
+      rc = launch_pdl(attention_kernel<128>, dim3(H, (M + kAttnTokens - 1) / kAttnTokens), dim3(kAttnWarps * 32),
+                      attn_smem, st, aa);
+    else
+      rc = launch_pdl(attention_kernel<64>, dim3(H, (M + kAttnTokens - 1) / kAttnTokens), dim3(kAttnWarps * 32),
+                      attn_smem, st, aa);
     if (rc) return rc;
     g_prof.mark(OP_ATTN, st);
     EpiArgs r{};
@@ -579,7 +528,6 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   }
   const size_t T = static_cast<size_t>(c.max_tokens);
   const size_t wide = std::max<size_t>(std::max<size_t>(c.d_model, c.ffn), static_cast<size_t>(c.n_heads) * c.head_dim);
-  m->max_chunks = (c.max_seq + kAttnChunk - 1) / kAttnChunk;
   auto fail = [&](cudaError_t e) {
     set_error(std::string("pearl_llama_create: ") + cudaGetErrorString(e));
     delete m;
@@ -591,12 +539,12 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   if ((e = cudaMalloc(&m->q, T * c.n_heads * c.head_dim * sizeof(bf16)))) return fail(e);
   if ((e = cudaMalloc(&m->o, T * c.n_heads * c.head_dim * sizeof(bf16)))) return fail(e);
   if ((e = cudaMalloc(&m->act, T * c.ffn * sizeof(bf16)))) return fail(e);
-  if ((e = cudaMalloc(&m->attn_part, T * c.n_heads * m->max_chunks * (c.head_dim + 2) * sizeof(float)))) return fail(e);
-  if ((e = cudaMalloc(&m->attn_flags, c.n_heads * sizeof(int)))) return fail(e);
-  if ((e = cudaMemset(m->attn_flags, 0, c.n_heads * sizeof(int)))) return fail(e);
   std::call_once(g_attn_once, [] {
-    g_attn_err = cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    g_attn_err = cudaFuncSetAttribute(attention_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(attention_smem_bytes(64, 128)));
+    if (g_attn_err == cudaSuccess)
+      g_attn_err = cudaFuncSetAttribute(attention_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(attention_smem_bytes(64, 64)));
   });
   if (g_attn_err) return fail(g_attn_err);
   if (c.gemm_kind == PEARL_GEMM_TCGEN05) {
@@ -618,8 +566,6 @@ extern "C" int pearl_llama_destroy(void* handle) {
   cudaFree(m->q);
   cudaFree(m->o);
   cudaFree(m->act);
-  cudaFree(m->attn_part);
-  cudaFree(m->attn_flags);
   tc_free(m->tc);
   delete m;
   return PEARL_OK;
