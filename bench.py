@@ -376,8 +376,8 @@ def main():
     ap.add_argument("--branch-std", type=float, default=5e-4)
     ap.add_argument("--kappa", type=float, default=13.0)
     ap.add_argument("--gemm-target", default="tcgen05")
-    ap.add_argument("--cpu-new", type=int, default=4)
-    ap.add_argument("--cpu-prompt", type=int, default=32)
+    ap.add_argument("--cpu-new", type=int, default=16)
+    ap.add_argument("--cpu-prompt", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
