@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(AttnArgs a) 
   float* st_all = reinterpret_cast<float*>(attn_smem);
   float* st = st_all + static_cast<size_t>(warp) * MT * (HD + 2);
   bf16* Qs = reinterpret_cast<bf16*>(st_all + static_cast<size_t>(kAttnWarps) * kAttnTokens * (HD + 2));  // [MT][HD]
+  bf16* Vw = Qs + kAttnTokens * HD + static_cast<size_t>(warp) * kAttnLanesPos * HD;  // this warp's V chunk
   for (int i = threadIdx.x; i < MT * HD / 8; i += blockDim.x) {
     const int t = i / (HD / 8), v = i % (HD / 8);
     reinterpret_cast<uint4*>(Qs + t * HD)[v] =
@@ -316,7 +317,14 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(AttnArgs a) 
 #pragma unroll
     for (int v = 0; v < HD / 8; ++v)
       kr[v] = have ? *reinterpret_cast<const uint4*>(a.kc + j * kstride + kvh * HD + v * 8) : make_uint4(0, 0, 0, 0);
-    // V slice (PER dims of every position of the chunk) is read per step below
+    // stage the chunk's V rows once (coalesced 16-byte loads), reused by every token
+    for (int i = lane; i < kAttnLanesPos * HD / 8; i += 32) {
+      const int jj = i / (HD / 8), v = i % (HD / 8);
+      const int jp = c * kAttnLanesPos + jj;
+      reinterpret_cast<uint4*>(Vw + jj * HD)[v] =
+          jp < ctx_max ? *reinterpret_cast<const uint4*>(a.vc + jp * kstride + kvh * HD + v * 8) : make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
     for (int t = 0; t < MT; ++t) {
       const int pt = p0 + t;
       if (c * kAttnLanesPos > pt) continue;  // chunk lies beyond this token's causal range
@@ -351,9 +359,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(AttnArgs a) 
 #pragma unroll
       for (int e = 0; e < PER; ++e) ov[e] = 0.f;
       const int jn = min(kAttnLanesPos, pt + 1 - c * kAttnLanesPos);
+#pragma unroll 8
       for (int jj = 0; jj < jn; ++jj) {
         const float pj = __shfl_sync(0xffffffffu, p, jj);
-        const bf16* vr = a.vc + (c * kAttnLanesPos + jj) * kstride + kvh * HD + lane * PER;
+        const bf16* vr = Vw + jj * HD + lane * PER;
         if (PER == 4) {
           const uint2 vv = *reinterpret_cast<const uint2*>(vr);
           ov[0] = fmaf(pj, __uint_as_float(vv.x << 16), ov[0]);
@@ -375,6 +384,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(AttnArgs a) 
       }
       __syncwarp();
     }
+    __syncwarp();  // Vw is overwritten by the warp's next chunk
   }
   __syncthreads();
   // merge the warps' states in warp order
@@ -398,7 +408,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(AttnArgs a) 
 }
 
 size_t attention_smem_bytes(int, int hd) {
-  return static_cast<size_t>(kAttnWarps) * kAttnTokens * (hd + 2) * 4 + static_cast<size_t>(kAttnTokens) * hd * 2 + 64;
+  return static_cast<size_t>(kAttnWarps) * kAttnTokens * (hd + 2) * 4 + static_cast<size_t>(kAttnTokens) * hd * 2 +
+         static_cast<size_t>(kAttnWarps) * kAttnLanesPos * hd * 2 + 64;
 }
 
 // ---------------------------------------------------------------------------
