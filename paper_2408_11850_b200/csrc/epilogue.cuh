@@ -30,13 +30,6 @@ struct EpiArgs {
   int n_kv;         // KV * hd
   int hd;
   int ld;           // leading dimension of out
-  // optional fused RMSNorm of the residual stream after a RESID GEMM (tcgen05
-  // path): the CTA that finishes the last tile writes
-  // norm_out[t] = bf16(out_f32[t] * rsqrt(mean(out_f32[t]^2) + eps) * norm_g)
-  const float* norm_g;
-  bf16* norm_out;
-  int* grid_flag;   // completed-tile counter (self-resetting)
-  float norm_eps;
 };
 
 // Handle four consecutive output rows n0..n0+3 (n0 % 4 == 0) for token t.

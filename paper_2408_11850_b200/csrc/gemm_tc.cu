@@ -144,45 +144,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
 
-// RMSNorm of M rows of length d by the 4 epilogue warps (warp w: tokens
-// t = w, w+4, ...).  Per token a fixed-order reduction: lane-strided float4
-// partial sums in k order, then an xor tree -- the same arithmetic whatever M.
-__device__ void fused_rmsnorm_rows(const EpiArgs& e, int M, int d, int et) {
-  const int w = et >> 5, lane = et & 31;
-  const int nv = d / 4;  // float4 per row
-  for (int t = w; t < M; t += 4) {
-    const float4* hr = reinterpret_cast<const float4*>(e.out_f32 + static_cast<size_t>(t) * d);
-    float ss = 0.f;
-    for (int b0 = 0; b0 < nv; b0 += 32 * 16) {
-      float4 v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int j = b0 + lane + 32 * i;
-        v[i] = j < nv ? __ldcg(hr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        ss = fmaf(v[i].x, v[i].x, ss);
-        ss = fmaf(v[i].y, v[i].y, ss);
-        ss = fmaf(v[i].z, v[i].z, ss);
-        ss = fmaf(v[i].w, v[i].w, ss);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    const float rs = 1.0f / sqrtf(ss / static_cast<float>(d) + e.norm_eps);
-    const float4* g4 = reinterpret_cast<const float4*>(e.norm_g);
-    uint2* xr = reinterpret_cast<uint2*>(e.norm_out + static_cast<size_t>(t) * d);
-    for (int j = lane; j < nv; j += 32) {
-      const float4 hv = __ldcg(hr + j);
-      const float4 gg = g4[j];
-      const __nv_bfloat162 lo = __floats2bfloat162_rn(hv.x * rs * gg.x, hv.y * rs * gg.y);
-      const __nv_bfloat162 hi = __floats2bfloat162_rn(hv.z * rs * gg.z, hv.w * rs * gg.w);
-      xr[j] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
-    }
-  }
-}
-
 __device__ __forceinline__ void unit_range(const TcArgs& a, int u, int& tile, int& split, int& kb0, int& kb1) {
   tile = u / a.S;
   split = u % a.S;
@@ -391,22 +352,6 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         epilogue4(a.e, t, n0, w, a.N);
       }
       epi_bar();
-      if (a.e.norm_g != nullptr) {
-        // this tile is final: count it; the CTA completing the last tile
-        // normalises the updated residual rows for the next GEMM
-        if (et == 0) {
-          int old;
-          asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.e.grid_flag) : "memory");
-          *s_last = (old == (a.N + kTileN - 1) / kTileN - 1);
-        }
-        epi_bar();
-        if (*s_last) {
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          fused_rmsnorm_rows(a.e, a.M, a.N, et);
-          if (et == 0) *a.e.grid_flag = 0;
-        }
-        epi_bar();
-      }
     }
   }
   __syncwarp();
@@ -524,18 +469,14 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   PEARL_CUDA_TRY(cudaMalloc(&ctx.partials, pf * sizeof(float)));
   PEARL_CUDA_TRY(cudaMalloc(&ctx.tile_flags, static_cast<size_t>(flags) * sizeof(int)));
   PEARL_CUDA_TRY(cudaMemset(ctx.tile_flags, 0, static_cast<size_t>(flags) * sizeof(int)));
-  PEARL_CUDA_TRY(cudaMalloc(&ctx.grid_flag, sizeof(int)));
-  PEARL_CUDA_TRY(cudaMemset(ctx.grid_flag, 0, sizeof(int)));
   return get_encoder();
 }
 
 void tc_free(TcGemmCtx& ctx) {
   if (ctx.partials) cudaFree(ctx.partials);
   if (ctx.tile_flags) cudaFree(ctx.tile_flags);
-  if (ctx.grid_flag) cudaFree(ctx.grid_flag);
   ctx.partials = nullptr;
   ctx.tile_flags = nullptr;
-  ctx.grid_flag = nullptr;
 }
 
 int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int M, int N, int K, const EpiArgs& e,
@@ -566,7 +507,6 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.KB = (K + kTileK - 1) / kTileK;
   a.S = force_splits > 0 ? force_splits : tc_splits(N, K, ctx.num_sms);
   a.e = e;
-  if (a.e.norm_g != nullptr) a.e.grid_flag = ctx.grid_flag;
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;
   const int tiles = (N + kTileN - 1) / kTileN;

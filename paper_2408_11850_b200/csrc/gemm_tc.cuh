@@ -29,7 +29,6 @@ struct TcWeightMap {
 struct TcGemmCtx {
   float* partials = nullptr;   // fp32 split-K partial tiles
   int* tile_flags = nullptr;   // arrival counters (self-resetting)
-  int* grid_flag = nullptr;    // completed-tile counter for fused norms (self-resetting)
   size_t partial_floats = 0;
   int n_flags = 0;
   int max_tokens = 0;

@@ -439,19 +439,11 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   const size_t layer_kv = static_cast<size_t>(c.max_seq) * nkv;
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
   const size_t attn_smem = attention_smem_bytes(M, hd);
-  const bool tc = c.gemm_kind == PEARL_GEMM_TCGEN05;
-  // tcgen05 path: the residual GEMMs (O, down) normalise their output for the
-  // next GEMM (fused RMSNorm); only layer 0's input norm is a separate kernel.
-  rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, m.layers[0].attn_norm, m.x, d, c.norm_eps, 0);
-  if (rc) return rc;
-  g_prof.mark(OP_NORM, st);
   for (int l = 0; l < c.n_layers; ++l) {
     const LayerW& L = m.layers[l];
-    if (l > 0 && !tc) {
-      rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
-      if (rc) return rc;
-      g_prof.mark(OP_NORM, st);
-    }
+    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
+    if (rc) return rc;
+    g_prof.mark(OP_NORM, st);
     EpiArgs e{};
     e.kind = EPI_QKV;
     e.out_bf16 = m.q;
@@ -480,19 +472,12 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     r.kind = EPI_RESID;
     r.out_f32 = m.h;
     r.ld = d;
-    if (tc) {
-      r.norm_g = L.mlp_norm;
-      r.norm_out = m.x;
-      r.norm_eps = c.norm_eps;
-    }
     rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
     if (rc) return rc;
     g_prof.mark(OP_O, st);
-    if (!tc) {
-      rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
-      if (rc) return rc;
-      g_prof.mark(OP_NORM, st);
-    }
+    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
+    if (rc) return rc;
+    g_prof.mark(OP_NORM, st);
     EpiArgs g{};
     g.kind = EPI_SWIGLU;
     g.out_bf16 = m.act;
@@ -500,29 +485,21 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     rc = launch_gemm(m, L.wgu, m.x, M, 2 * c.ffn, d, g, st);
     if (rc) return rc;
     g_prof.mark(OP_GU, st);
-    EpiArgs r2 = r;
-    if (tc) r2.norm_g = (l + 1 < c.n_layers) ? m.layers[l + 1].attn_norm : m.final_norm;
-    rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r2, st);
+    rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r, st);
     if (rc) return rc;
     g_prof.mark(OP_DOWN, st);
   }
   if (!want_logits) return PEARL_OK;
   const int first = logits_all ? 0 : M - 1;
   const int rows = M - first;
-  const bf16* xin = m.x;
-  if (tc) {
-    xin = m.x + static_cast<size_t>(first) * d;  // final norm fused into the last down GEMM
-  } else {
-    rc = launch_pdl(rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, st, m.h, m.final_norm, m.x, d, c.norm_eps,
-                    first);
-    if (rc) return rc;
-    g_prof.mark(OP_NORM, st);
-  }
+  rc = launch_pdl(rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, st, m.h, m.final_norm, m.x, d, c.norm_eps, first);
+  if (rc) return rc;
+  g_prof.mark(OP_NORM, st);
   EpiArgs s{};
   s.kind = EPI_STORE_F32;
   s.out_f32 = logits;
   s.ld = c.vocab;
-  rc = launch_gemm(m, m.lm_head, xin, rows, c.vocab, d, s, st);
+  rc = launch_gemm(m, m.lm_head, m.x, rows, c.vocab, d, s, st);
   g_prof.mark(OP_HEAD, st);
   return rc;
 }
