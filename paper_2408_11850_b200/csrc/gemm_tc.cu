@@ -62,7 +62,10 @@ struct TcCfg {
 };
 
 struct TcArgs {
-  int M, N, K, KB, S, units;
+  int M, N, K, KB;
+  long long T;   // total (tile, k-block) iterations
+  int G;         // CTAs sharing them (stream-K); a function of (N, K) only
+  int seg_max;   // partial slots per tile
   EpiArgs e;
   float* partials;
   int* flags;
@@ -144,11 +147,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
 
-__device__ __forceinline__ void unit_range(const TcArgs& a, int u, int& tile, int& split, int& kb0, int& kb1) {
-  tile = u / a.S;
-  split = u % a.S;
-  kb0 = static_cast<int>((static_cast<long long>(split) * a.KB) / a.S);
-  kb1 = static_cast<int>((static_cast<long long>(split + 1) * a.KB) / a.S);
+// Stream-K: CTA c owns iterations [c*T/G, (c+1)*T/G) of the flattened
+// (tile, k-block) space.  cta_of(x) is the CTA whose range contains x.
+__device__ __forceinline__ int cta_of(const TcArgs& a, long long x) {
+  return static_cast<int>(((x + 1) * a.G + a.T - 1) / a.T) - 1;
+}
+
+struct Unit {
+  int tile, kb0, kb1, seg, nseg;
+};
+
+// The unit (maximal run inside one tile) starting at iteration x, capped at r1.
+__device__ __forceinline__ Unit unit_at(const TcArgs& a, long long x, long long r1) {
+  Unit u;
+  u.tile = static_cast<int>(x / a.KB);
+  u.kb0 = static_cast<int>(x % a.KB);
+  u.kb1 = static_cast<int>(min(static_cast<long long>(a.KB), u.kb0 + (r1 - x)));
+  const long long t0 = static_cast<long long>(u.tile) * a.KB;
+  const int c0 = cta_of(a, t0);
+  u.seg = cta_of(a, x) - c0;
+  u.nseg = cta_of(a, t0 + a.KB - 1) - c0 + 1;
+  return u;
 }
 
 // ---- kernel ------------------------------------------------------------------
@@ -171,8 +190,9 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // units of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
-  const int my_units = a.units > static_cast<int>(blockIdx.x) ? (a.units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long r0 = static_cast<long long>(blockIdx.x) * a.T / a.G;
+  const long long r1 = static_cast<long long>(blockIdx.x + 1) * a.T / a.G;
+  const int total = static_cast<int>(r1 - r0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
@@ -203,64 +223,46 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---- TMA producer: iteration it walks (unit, k-block) in order
-      int total = 0;
-      for (int ui = 0; ui < my_units; ++ui) {
-        int t, sp, k0, k1;
-        unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
-        total += k1 - k0;
-      }
+      // ---- TMA producer: iterations r0..r1 in order (tile = x / KB, kb = x % KB)
       const uint32_t bytes = stage_bytes;
       const int npre = min(stages, total);
       // W does not depend on the previous kernel: request it before the PDL wait
-      int ui = 0, t = 0, sp = 0, k0 = 0, k1 = 0, kb = 0;
-      if (my_units > 0) {
-        unit_range(a, blockIdx.x, t, sp, k0, k1);
-        kb = k0;
-      }
-      int pre_k[kMaxStages];
       for (int it = 0; it < npre; ++it) {
+        const long long x = r0 + it;
         unsigned char* st = smem + it * stage_bytes;
         mbar_expect_tx(&full[it], bytes);
-        tma_load_2d(st, &tmW, &full[it], kb * kTileK, t * kTileN);
-        pre_k[it] = kb;
-        if (++kb == k1 && ++ui < my_units) {
-          unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
-          kb = k0;
-        }
+        tma_load_2d(st, &tmW, &full[it], static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN);
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int it = 0; it < npre; ++it) {
+        const long long x = r0 + it;
         unsigned char* st = smem + it * stage_bytes;
         for (int j = 0; j < NT; ++j)
-          tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[it], pre_k[it] * kTileK, j * kTokTile);
+          tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[it], static_cast<int>(x % a.KB) * kTileK, j * kTokTile);
       }
       for (int it = npre; it < total; ++it) {
+        const long long x = r0 + it;
         const int s = it % stages;
         mbar_wait(&empty[s], ((it / stages) - 1) & 1);
         unsigned char* st = smem + s * stage_bytes;
+        const int kc = static_cast<int>(x % a.KB) * kTileK;
         mbar_expect_tx(&full[s], bytes);
-        tma_load_2d(st, &tmW, &full[s], kb * kTileK, t * kTileN);
-        for (int j = 0; j < NT; ++j)
-          tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kb * kTileK, j * kTokTile);
-        if (++kb == k1 && ++ui < my_units) {
-          unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
-          kb = k0;
-        }
+        tma_load_2d(st, &tmW, &full[s], kc, static_cast<int>(x / a.KB) * kTileN);
+        for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---- MMA issuer
-      int it = 0;
-      for (int ui = 0; ui < my_units; ++ui) {
-        int t, sp, k0, k1;
-        unit_range(a, blockIdx.x + ui * gridDim.x, t, sp, k0, k1);
+      // ---- MMA issuer: one accumulator per unit (run of k-blocks inside a tile)
+      int it = 0, ui = 0;
+      for (long long x = r0; x < r1; ++ui) {
+        const Unit u = unit_at(a, x, r1);
+        x += u.kb1 - u.kb0;
         const int b = ui % kAccs;
         if (ui >= kAccs) mbar_wait(&acc_empty[b], ((ui / kAccs) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + b * NT * kTokTile;
-        for (int kb = k0; kb < k1; ++kb, ++it) {
+        for (int kb = u.kb0; kb < u.kb1; ++kb, ++it) {
           const int s = it % stages;
           mbar_wait(&full[s], (it / stages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
             const uint64_t bdesc = umma_desc_sw128(st + kWBytes + j * kXBytes);
 #pragma unroll
             for (int kk = 0; kk < kTileK / 16; ++kk)
-              umma_bf16(acc + j * kTokTile, adesc + 2 * kk, bdesc + 2 * kk, (kb > k0 || kk > 0) ? 1u : 0u);
+              umma_bf16(acc + j * kTokTile, adesc + 2 * kk, bdesc + 2 * kk, (kb > u.kb0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
         }
@@ -283,9 +285,11 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
     const int row = lanegrp * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127
     const int Mp = (a.M + 3) & ~3;  // partial row stride (float4 aligned)
-    for (int ui = 0; ui < my_units; ++ui) {
-      int tile, split, k0, k1;
-      unit_range(a, blockIdx.x + ui * gridDim.x, tile, split, k0, k1);
+    int ui = 0;
+    for (long long x = r0; x < r1; ++ui) {
+      const Unit u = unit_at(a, x, r1);
+      x += u.kb1 - u.kb0;
+      const int tile = u.tile;
       const int b = ui % kAccs;
       mbar_wait(&acc_full[b], (ui / kAccs) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -295,13 +299,13 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * NT * kTokTile + j * kTokTile, v + 16 * j);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&acc_empty[b]);  // the MMA warp may reuse this accumulator
-      if (a.S == 1) {
+      if (u.nseg == 1) {
 #pragma unroll
         for (int q = 0; q < NT * 4; ++q)
           *reinterpret_cast<float4*>(E + row * ES + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       } else {
         // this split's fp32 partial row: Mp contiguous floats (float4 stores)
-        float* dst = a.partials + ((static_cast<size_t>(tile) * a.S + split) * kTileN + row) * Mp;
+        float* dst = a.partials + ((static_cast<size_t>(tile) * a.seg_max + u.seg) * kTileN + row) * Mp;
 #pragma unroll
         for (int q = 0; q < NT * 4; ++q)
           if (4 * q < Mp)
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         if (et == 0) {
           int old;
           asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.flags + tile) : "memory");
-          *s_last = (old == a.S - 1);
+          *s_last = (old == u.nseg - 1);
         }
         epi_bar();
         if (!*s_last) continue;
@@ -318,18 +322,18 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         // Fixed split order => independent of arrival order and of M.  Each
         // thread owns one row; per 4-token quad all S float4 loads are in
         // flight together, then summed in split order.
-        const float* src = a.partials + (static_cast<size_t>(tile) * a.S * kTileN + row) * Mp;
+        const float* src = a.partials + (static_cast<size_t>(tile) * a.seg_max * kTileN + row) * Mp;
         const size_t sstride = static_cast<size_t>(kTileN) * Mp;
         for (int q = 0; q < Mp / 4; ++q) {
           float4 p[16];
           float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int s0 = 0; s0 < a.S; s0 += 16) {
+          for (int s0 = 0; s0 < u.nseg; s0 += 16) {
 #pragma unroll
             for (int s = 0; s < 16; ++s)
-              if (s0 + s < a.S) p[s] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + s) * sstride + 4 * q));
+              if (s0 + s < u.nseg) p[s] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + s) * sstride + 4 * q));
 #pragma unroll
             for (int s = 0; s < 16; ++s)
-              if (s0 + s < a.S) {
+              if (s0 + s < u.nseg) {
                 acc.x += p[s].x;
                 acc.y += p[s].y;
                 acc.z += p[s].z;
@@ -432,6 +436,18 @@ int tc_splits(int N, int K, int num_sms) {
   return best;
 }
 
+// Largest number of stream-K segments any tile is cut into.
+int tc_seg_max(int tiles, int KB, int G) {
+  const long long T = static_cast<long long>(tiles) * KB;
+  auto cta_of = [&](long long x) { return static_cast<int>(((x + 1) * G + T - 1) / T) - 1; };
+  int mx = 1;
+  for (int t = 0; t < tiles; ++t) {
+    const long long t0 = static_cast<long long>(t) * KB;
+    mx = std::max(mx, cta_of(t0 + KB - 1) - cta_of(t0) + 1);
+  }
+  return mx;
+}
+
 int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   if (c.max_tokens > kMaxTokTiles * kTokTile) {
     set_error("tcgen05 path supports max_tokens <= 64");
@@ -458,9 +474,10 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   size_t pf = 0;
   int flags = 0;
   for (auto& s : shapes) {
-    const int S = tc_splits(s[0], s[1], ctx.num_sms);
     const int tiles = (s[0] + kTileN - 1) / kTileN;
-    const int Sa = std::max(S, ctx.min_plan_splits);
+    const int KB = (s[1] + kTileK - 1) / kTileK;
+    int Sa = tc_seg_max(tiles, KB, std::min<long long>(ctx.num_sms, static_cast<long long>(tiles) * KB));
+    Sa = std::max(Sa, ctx.min_plan_splits);
     pf = std::max(pf, static_cast<size_t>(tiles) * Sa * kTileN * kMaxTokTiles * kTokTile);
     flags = std::max(flags, tiles);
   }
@@ -505,20 +522,21 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.N = N;
   a.K = K;
   a.KB = (K + kTileK - 1) / kTileK;
-  a.S = force_splits > 0 ? force_splits : tc_splits(N, K, ctx.num_sms);
+  const int tiles = (N + kTileN - 1) / kTileN;
+  a.T = static_cast<long long>(tiles) * a.KB;
+  a.G = static_cast<int>(std::min<long long>(force_splits > 0 ? force_splits : ctx.num_sms, a.T));
+  a.seg_max = tc_seg_max(tiles, a.KB, a.G);
   a.e = e;
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;
-  const int tiles = (N + kTileN - 1) / kTileN;
-  a.units = tiles * a.S;
-  if (a.S > 32 || static_cast<size_t>(tiles) * a.S * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
+  if (static_cast<size_t>(tiles) * a.seg_max * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
       tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");
     return PEARL_ERR_ARG;
   }
   const int NT = (M + kTokTile - 1) / kTokTile;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(std::min(a.units, ctx.num_sms));
+  cfg.gridDim = dim3(a.G);
   cfg.blockDim = dim3(kTcThreads);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

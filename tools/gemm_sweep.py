@@ -1,4 +1,4 @@
-"""Back-to-back timing of the tcgen05 GEMM for a shape over split factors and M."""
+"""Back-to-back timing of the tcgen05 GEMM (stream-K) for a shape over grid sizes G and M."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -11,7 +11,7 @@ for M in (1, 4, 16):
     X = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     Y = torch.empty(M, N, device="cuda")
     res = []
-    for S in (1, 2, 4, 8, 13, 16, 0):
+    for S in (74, 96, 128, 148, 0):
         f = lambda: lib.pearl_gemm(1, W.data_ptr(), X.data_ptr(), Y.data_ptr(), M, N, K, S, st)
         for _ in range(3): f()
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -19,5 +19,5 @@ for M in (1, 4, 16):
         for _ in range(20): f()
         e.record(); e.synchronize()
         t = s.elapsed_time(e) / 20 * 1e3
-        res.append(f"S={S if S else 'auto(' + str(lib.pearl_gemm_splits(N, K)) + ')'}:{t:.1f}us/{N*K*2/t/1e3:.0f}GB/s")
+        res.append(f"G={S if S else 'auto'}:{t:.1f}us/{N*K*2/t/1e3:.0f}GB/s")
     print(f"N={N} K={K} M={M}: " + "  ".join(res), flush=True)
