@@ -136,14 +136,16 @@ def run_gpu(args):
 
     def run(kind, i):
         if kind == "pearl":
-            return pk.decode_pearl(draft, target, prompts[i], cfg_for(pearl_gamma, 17 + i, args.adaptive))
+            return pk.decode_pearl(draft, target, prompts[i], cfg_for(pearl_gamma, 17 + i, not args.fixed_gamma))
         if kind == "sd":
             return pk.decode_sd(draft, target, prompts[i], cfg_for(args.sd_gamma, 17 + i))
+        if kind in ("sd8", "sd16"):
+            return pk.decode_sd(draft, target, prompts[i], cfg_for(int(kind[2:]), 17 + i))
         return pk.decode_autoregressive(target, prompts[i], cfg_for(1, 17 + i))
 
     results = {}
     clocks = None
-    for kind in ("ar", "sd", "pearl"):  # PEARL last: its clocks are sampled
+    for kind in ("ar", "sd", "sd8", "sd16", "pearl"):  # PEARL last: its clocks are sampled
         for i in range(args.warmup):
             run(kind, i)
         torch.cuda.synchronize()
@@ -169,6 +171,7 @@ def run_gpu(args):
                              mean_tok_per_fwd=pk.mean_tokens_per_target_forward(steps),
                              alpha=pk.empirical_acceptance(steps) if kind != "ar" else None,
                              gamma=res[0].stats.get("gamma"),
+                             gammas=sorted(set(g for r in res for g in r.stats.get("gammas", []))),
                              fallbacks=sum(r.stats.get("fallbacks", 0) for r in res))
     # max over ranks of the timed region, sum of tokens
     agg = {}
@@ -184,7 +187,7 @@ def run_gpu(args):
         else:
             agg[kind] = tuple(vals.tolist())
     # roofline of the dominant kernel sequence: one target window forward
-    rl = roofline(target, draft, pearl_gamma if not args.adaptive else results["pearl"]["gamma"], args)
+    rl = roofline(target, draft, args.gamma, args)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(target, draft, prompts[0], args, greedy, temp)
@@ -214,7 +217,8 @@ def run_gpu(args):
             "workload": f"{args.pair} PEARL, batch 1, prompt {args.prompt}, {args.new} new tokens, "
                         f"{'greedy T=0' if greedy else f'T={temp}'}, draft+target co-resident per GPU",
             "pair": args.pair, "global_batch": ws, "prompt_len": args.prompt, "new_tokens": args.new,
-            "gamma": results["pearl"]["gamma"], "adaptive_gamma": bool(args.adaptive),
+            "gamma": results["pearl"]["gammas"] if not args.fixed_gamma else args.gamma,
+            "adaptive_gamma": not args.fixed_gamma,
             "sd_gamma": args.sd_gamma, "temperature": 0.0 if greedy else temp,
             "target_gemm": args.gemm_target, "parallelism": f"replicas x{ws}",
             "l2": "weights 13.6 GB >> 126 MB L2: every forward streams HBM (no flush needed)",
@@ -226,6 +230,10 @@ def run_gpu(args):
         "sd_tokens_per_s": round(ts_ / ds_, 2),
         "speedup_vs_ar": round((tp / dp) / (ta / da), 3),
         "speedup_vs_sd": round((tp / dp) / (ts_ / ds_), 3),
+        "sd_best_tokens_per_s": round(max(agg[k][3] / agg[k][0] for k in ("sd", "sd8", "sd16")), 2),
+        "sd_by_gamma_tokens_per_s": {str(args.sd_gamma): round(ts_ / ds_, 2),
+                                     "8": round(agg["sd8"][3] / agg["sd8"][0], 2),
+                                     "16": round(agg["sd16"][3] / agg["sd16"][0], 2)},
         "e2e_speedup_vs_ar": round((tp / ep) / (ta / ea), 3),
         "mean_accepted_tokens_per_target_fwd": round(results["pearl"]["mean_tok_per_fwd"], 3),
         "sd_mean_tokens_per_target_fwd": round(results["sd"]["mean_tok_per_fwd"], 3),
@@ -369,7 +377,7 @@ def main():
     ap.add_argument("--gamma", type=int, default=4)
     ap.add_argument("--sd-gamma", type=int, default=4)
     ap.add_argument("--gamma-max", type=int, default=32)
-    ap.add_argument("--adaptive", action="store_true")
+    ap.add_argument("--fixed-gamma", action="store_true", help="PEARL with fixed --gamma instead of adaptive")
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--new", type=int, default=128)
     ap.add_argument("--temperature", type=float, default=1.0)

@@ -304,17 +304,73 @@ def _seq0(model: LlamaModel, prefix: Sequence[int]) -> List[int]:
     return [model.bos_id] + [int(t) for t in prefix]
 
 
+def pearl_tokens_per_step(alpha: float, gamma: int) -> float:
+    """Stationary mean tokens finalised per PEARL step under the reference's
+    semantics (pre-verify finalises exactly 1, engines.py:453; post-verify
+    finalises the accepted chain + correction or gamma, engines.py:500-515):
+    E = (1 - a^g) / ((1 - a)(1 - a^g + a)) -- the two-state Markov chain over
+    PRE/POST modes.  alpha -> 1 gives gamma."""
+    a = min(max(alpha, 1e-6), 1.0 - 1e-9)
+    ag = a ** gamma
+    return (1.0 - ag) / ((1.0 - a) * (1.0 - ag + a))
+
+
+class _GammaPlanner:
+    """Adaptive draft length (paper §3.4): gamma maximising expected PEARL
+    tokens per unit step time, E(gamma, alpha_hat) / max(t_target(gamma),
+    gamma * t_draft), with t measured once per model pair (CUDA events) and
+    alpha_hat a running Laplace estimate of this decode's acceptance.  The
+    choice depends only on the decode's own history and the cached
+    calibration, so a decode is reproducible within a process."""
+
+    GRID = (1, 2, 3, 4, 6, 8, 12, 16, 20, 24, 32, 48, 64)
+
+    def __init__(self, target: LlamaModel, draft: LlamaModel, gamma_max: int, gamma0: int):
+        key = "_pearl_calib_" + str(id(draft))
+        cal = target.__dict__.get(key)
+        if cal is None:
+            t_d = draft.measure_forward_time(1) + 6e-6  # + the pick kernel
+            ms = [1, 8, 16, 32]
+            t_t = {m: target.measure_forward_time(m) for m in ms}
+            cal = (t_d, t_t)
+            target.__dict__[key] = cal
+        self.t_d, self.t_t = cal
+        self.gmax = gamma_max
+        self.acc, self.exam = 3.0, 4.0  # prior alpha 0.75
+        self.gamma = gamma0
+
+    def _t_target(self, m: int) -> float:
+        ks = sorted(self.t_t)
+        if m <= ks[0]:
+            return self.t_t[ks[0]]
+        for lo, hi in zip(ks, ks[1:]):
+            if m <= hi:
+                w = (m - lo) / (hi - lo)
+                return (1 - w) * self.t_t[lo] + w * self.t_t[hi]
+        return self.t_t[ks[-1]] * m / ks[-1]
+
+    def observe(self, accepted: int, rejected: int) -> None:
+        self.acc += accepted
+        self.exam += accepted + rejected
+
+    def next_gamma(self) -> int:
+        alpha = self.acc / self.exam
+        best, best_rate = 1, -1.0
+        for g in self.GRID:
+            if g > self.gmax:
+                break
+            rate = pearl_tokens_per_step(alpha, g) / max(self._t_target(g), g * self.t_d)
+            if rate > best_rate:
+                best, best_rate = g, rate
+        self.gamma = best
+        return best
+
+
 def choose_gamma(cfg, target: LlamaModel, draft: LlamaModel) -> int:
-    """Adaptive draft length gamma = round(c), c = t_target / t_draft (paper §3.4;
-    theory.pearl_optimal_gamma), measured once per pair."""
+    """Initial draft length: cfg.gamma, or the planner's choice under adaptive_gamma."""
     if not cfg.adaptive_gamma:
         return cfg.gamma
-    key = "_pearl_c_" + str(id(draft))
-    c = target.__dict__.get(key)
-    if c is None:
-        c = target.measure_forward_time(max(1, cfg.gamma)) / draft.measure_forward_time(1)
-        target.__dict__[key] = c
-    return int(max(1, min(cfg.gamma_max, round(c))))
+    return _GammaPlanner(target, draft, cfg.gamma_max, cfg.gamma).next_gamma()
 
 
 # -- engines ---------------------------------------------------------------
@@ -322,14 +378,15 @@ def choose_gamma(cfg, target: LlamaModel, draft: LlamaModel) -> int:
 
 def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], cfg, concurrent: bool = True):
     from .engines import DecodeResult, StepTrace, finalize_step
-    gamma = choose_gamma(cfg, target, draft)
+    planner = _GammaPlanner(target, draft, cfg.gamma_max, cfg.gamma) if cfg.adaptive_gamma else None
+    gamma = planner.next_gamma() if planner else cfg.gamma
     gmax = max(cfg.gamma_max, gamma, cfg.gamma)
-    t_d = gamma * draft.latency.forward_time  # (measured before the caches are filled)
+    t_d1 = draft.latency.forward_time  # (measured before the caches are filled)
     t_t = target.latency.forward_time
     rt = _runtime(target, draft, gmax)
     seq0 = _seq0(target, prefix)
     n0 = len(seq0)
-    stats = _new_stats(gamma=gamma)
+    stats = _new_stats(gamma=gamma, gammas=[])
     rt.reset(seq0, stats)
     root = RandomStream(cfg.seed)
     tab_d = _Tables(rt, rt.u_draft, None if cfg.greedy else root.split(0), S_DCUR)
@@ -345,6 +402,7 @@ def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], c
             raise ValueError("decode exceeds the KV-cache capacity (raise max_seq)")
         k = len(pending)
         m0 = len(committed) + k - dpos
+        stats["gammas"].append(gamma)
         key = ("pearl", k, gamma, m0, bool(cfg.greedy), invt, bool(concurrent))
         rt.replay(key, lambda: rt._pearl_body(k, gamma, m0, invt, cfg.greedy, concurrent), stats)
         s = rt.summary_host.numpy()
@@ -367,7 +425,10 @@ def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], c
         assert int(s[SUM_COMMITTED]) == len(committed)
         if kind == "pre_verify":
             acc = 1 if corr < 0 else 0
-        trace = StepTrace(len(steps), kind, tuple(xs), acc, cval, delta, t_d, t_t)
+        trace = StepTrace(len(steps), kind, tuple(xs), acc, cval, delta, gamma * t_d1, t_t)
+        if planner is not None:
+            planner.observe(acc, 0 if cval is None else 1)
+            gamma = planner.next_gamma()
         tab_v.advance(int(s[SUM_VCUR]), 2 * gmax + 8)
         tab_d.advance(int(s[SUM_DCUR]), 2 * gmax + 8)
         stop = finalize_step(tuple(committed), n0, produced, cfg)

@@ -147,3 +147,19 @@ def test_eos_and_truncation(pair):
         r = fn(pk.EngineConfig(gamma=4, max_new_tokens=7, seed=2, greedy=True))
         assert r.tokens == base.tokens[:7]
         assert sum(s.finalized_delta for s in r.steps) == 7
+
+
+def test_adaptive_gamma_replays_exactly(pair):
+    """Adaptive draft length: the per-step gammas the planner chose, replayed
+    through the restated reference loop, give the same tokens and traces."""
+    import paper_2408_11850_b200 as pk
+    from oracle import engine as oe
+    target, draft = pair
+    prefix = list(range(40, 60))
+    cfg = pk.EngineConfig(gamma=4, max_new_tokens=64, seed=9, adaptive_gamma=True, gamma_max=16)
+    res = pk.decode_pearl(draft, target, prefix, cfg)
+    sched = res.stats["gammas"]
+    assert len(sched) == len(res.steps) and all(1 <= g <= 16 for g in sched)
+    toks, steps = oe.decode_pearl(draft, target, prefix, 4, 64, 9, gamma_schedule=sched)
+    assert list(res.tokens) == list(toks)
+    assert _strip(res.steps) == steps
