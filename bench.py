@@ -174,18 +174,7 @@ def run_gpu(args):
                              gammas=sorted(set(g for r in res for g in r.stats.get("gammas", []))),
                              fallbacks=sum(r.stats.get("fallbacks", 0) for r in res))
     # max over ranks of the timed region, sum of tokens
-    agg = {}
-    for kind, r in results.items():
-        vals = torch.tensor([r["device_s"], r["event_s"], r["wall_s"], float(r["tokens"])], device="cuda",
-                            dtype=torch.float64)
-        if ws > 1:
-            mx = vals.clone()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            sm = vals.clone()
-            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-            agg[kind] = (mx[0].item(), mx[1].item(), mx[2].item(), sm[3].item())
-        else:
-            agg[kind] = tuple(vals.tolist())
+    agg = aggregate(results, ws)
     # roofline of the dominant kernel sequence: one target window forward
     rl = roofline(target, draft, args.gamma, args)
     cpu = None
@@ -250,6 +239,25 @@ def run_gpu(args):
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def aggregate(results, ws, device="cuda"):
+    """(max device s, max event s, max wall s, sum tokens) per engine over ranks."""
+    import torch
+    import torch.distributed as dist
+    agg = {}
+    for kind, r in results.items():
+        vals = torch.tensor([r["device_s"], r["event_s"], r["wall_s"], float(r["tokens"])], device=device,
+                            dtype=torch.float64)
+        if ws > 1:
+            mx = vals.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = vals.clone()
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            agg[kind] = (mx[0].item(), mx[1].item(), mx[2].item(), sm[3].item())
+        else:
+            agg[kind] = tuple(vals.tolist())
+    return agg
 
 
 def roofline(target, draft, gamma, args):

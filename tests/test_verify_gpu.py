@@ -188,3 +188,52 @@ def test_empirical_law_one_slot(pk):
             r = _verify(pk, [p_row], [q_row], [y], us[k, 1:])
             counts[y if r["accepted"] == 1 else r["correction"]] += 1
     np.testing.assert_allclose(counts / N, P, atol=0.015)
+
+
+@pytest.mark.parametrize("V", [32256, 128256])
+def test_large_vocab_against_oracle(pk, V):
+    """V beyond the reference's MAX_VOCAB (Llama-3: 128256, 16-CTA clusters):
+    K1 and the pick kernel against the oracle restatement of core.py/sampling.py
+    on the device law of the same logits and the same PCG64 uniforms."""
+    from oracle import engine as oe
+    from oracle.probdist import logits_to_probs, sample_index
+    n = 4
+    for seed in (1, 2, 3):
+        lp = recipes.make_logits(V, n, seed, scale=3.0)
+        lq = (lp + recipes.make_logits(V, n, seed + 100, scale=0.7)).astype(np.float32)  # correlated draft
+        P = [logits_to_probs(r)[0] for r in lp]
+        Qd = [logits_to_probs(r) for r in lq]
+        rd = oe.OracleStream(seed).split(0)
+        drafted = [sample_index(cdf, rd.uniform()) for _, cdf in Qd]
+        rv = oe.OracleStream(seed).split(1)
+        want = oe.verify_chain(drafted, [q for q, _ in Qd], P, rv)
+        us = pk.RandomStream(seed).split(1).peek(n + 1)
+        tp, tq = torch.from_numpy(lp).cuda(), torch.from_numpy(lq).cuda()
+        r = _verify(pk, [tp[i] for i in range(n)], [tq[i] for i in range(n)], drafted, us, mode=1, V=V)
+        got = (r["accepted"], None if r["correction"] < 0 else r["correction"], r["examined"])
+        assert r["status"] == 0 and got == want and r["draws"] == rv.n_draws, (V, seed, got, want)
+        # probs64 mode on the oracle's normalised rows gives the same verdict
+        r2 = _verify(pk, [torch.from_numpy(np.array(p)).cuda() for p in P],
+                     [torch.from_numpy(np.array(q)).cuda() for q, _ in Qd], drafted, us)
+        assert (r2["accepted"], r2["correction"], r2["draws"]) == (r["accepted"], r["correction"], r["draws"])
+    # inverse-CDF pick at adversarial uniforms (exact cdf values and neighbours)
+    from paper_2408_11850_b200 import _device, _lib
+    probs, cdf = logits_to_probs(recipes.make_logits(V, 1, 77, scale=2.0)[0])
+    rng = np.random.default_rng(5)
+    us = [0.0, float(np.nextafter(1.0, 0.0))]
+    for i in rng.choice(V - 1, 8, replace=False):
+        c = float(cdf[i])
+        us += [c, float(np.nextafter(c, 0.0)), float(np.nextafter(c, 2.0))]
+    us = [u for u in us if 0.0 <= u < 1.0]
+    row = torch.from_numpy(np.array(probs)).cuda()
+    rows = _device.row_ptrs([row] * len(us), torch.device("cuda"))
+    u = torch.tensor(us, dtype=torch.float64, device="cuda")
+    out = torch.empty(len(us), dtype=torch.int32, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    work = torch.zeros(65536, dtype=torch.uint8, device="cuda")
+    _lib.prepare_vocab(V)
+    _lib.check(_lib.load().pearl_sample_rows(0, _device.ptr(rows), len(us), V, _device.ptr(u), len(us), None, 1.0, 0,
+                                             _device.ptr(out), None, _device.ptr(st), _device.ptr(work),
+                                             _device.stream_ptr()))
+    assert int(st.item()) == 0
+    assert out.cpu().tolist() == [sample_index(cdf, x) for x in us]
