@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
 // ---------------------------------------------------------------------------
 constexpr int kAttnWarps = 8;
 constexpr int kAttnLanesPos = 32;  // positions per warp chunk
-constexpr int kAttnTokens = 16;    // window tokens per block (grid.y = ceil(M / 16))
+constexpr int kAttnTokens = 1;     // window tokens per block (grid.y = ceil(M / kAttnTokens))
 
 struct AttnArgs {
   const bf16* q;      // [M, H, hd]
@@ -283,7 +284,7 @@ struct AttnArgs {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kAttnWarps * 32) attention_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs a) {
   constexpr int PER = HD / 32;  // dims per lane (2 or 4)
   extern __shared__ __align__(16) unsigned char attn_smem[];
   pdl_wait();
@@ -423,13 +424,29 @@ int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs
                     M, N, K, e);
 }
 
+static int ablate_mask();
 int launch_gemm(Llama& m, const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st) {
+  if (ablate_mask() & 4) return PEARL_OK;
   if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st);
   return launch_gemv(W, X, M, N, K, e, st);
 }
 
+// Diagnostics only (PEARL_ABLATE=attn|norm|gemm): skip a kernel class to
+// measure its in-graph cost.  Results are wrong while set.
+static int ablate_mask() {
+  static const int m = [] {
+    const char* v = std::getenv("PEARL_ABLATE");
+    if (!v) return 0;
+    std::string s(v);
+    return (s.find("attn") != std::string::npos ? 1 : 0) | (s.find("norm") != std::string::npos ? 2 : 0) |
+           (s.find("gemm") != std::string::npos ? 4 : 0);
+  }();
+  return m;
+}
+
 int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_add, bool logits_all,
                   bool want_logits, float* logits, cudaStream_t st) {
+  const int abl = ablate_mask();
   const auto& c = m.cfg;
   const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads;
   const int nq = H * hd, nkv = KV * hd;
@@ -441,8 +458,10 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   const size_t attn_smem = attention_smem_bytes(M, hd);
   for (int l = 0; l < c.n_layers; ++l) {
     const LayerW& L = m.layers[l];
-    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
-    if (rc) return rc;
+    if (!(abl & 2)) {
+      rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
+      if (rc) return rc;
+    }
     g_prof.mark(OP_NORM, st);
     EpiArgs e{};
     e.kind = EPI_QKV;
@@ -460,7 +479,9 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     if (rc) return rc;
     g_prof.mark(OP_QKV, st);
     AttnArgs aa{m.q, e.kc, e.vc, m.o, pos, pos_add, M, H, KV, hd, scale};
-    if (hd == 128)
+    if (abl & 1)
+      rc = PEARL_OK;
+    else if (hd == 128)
       rc = launch_pdl(attention_kernel<128>, dim3(H, (M + kAttnTokens - 1) / kAttnTokens), dim3(kAttnWarps * 32),
                       attn_smem, st, aa);
     else
@@ -475,8 +496,10 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
     if (rc) return rc;
     g_prof.mark(OP_O, st);
-    rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
-    if (rc) return rc;
+    if (!(abl & 2)) {
+      rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
+      if (rc) return rc;
+    }
     g_prof.mark(OP_NORM, st);
     EpiArgs g{};
     g.kind = EPI_SWIGLU;
