@@ -203,11 +203,41 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
   }
 }
 
+// Optional fused RMSNorm of the input: when xh != nullptr the operand is
+// x[t] = bf16(xh[t] * rs[t] * ng), rs[t] = 1/sqrt(mean(xh[t]^2) + eps), with
+// rs computed by every block in the same fixed order (warp t%8 strides the
+// row with float4 loads, xor tree) -- identical in every block and for any M.
+struct GemvNorm {
+  const float* xh;  // [M, K] fp32 residual stream, or nullptr (X is bf16 input)
+  const float* g;   // [K] gain
+  float eps;
+};
+
+constexpr int kGemvMaxNormTok = 64;
+
 __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __restrict__ W, const bf16* __restrict__ X,
-                                                               int M, int N, int K, EpiArgs e) {
+                                                               int M, int N, int K, EpiArgs e, GemvNorm nrm) {
+  __shared__ float s_rs[kGemvMaxNormTok];
   pdl_wait();
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (nrm.xh != nullptr) {
+    for (int t = warp; t < M; t += kGemvWarps) {
+      const float4* hr = reinterpret_cast<const float4*>(nrm.xh + static_cast<size_t>(t) * K);
+      float ss = 0.f;
+      for (int j = lane; j < K / 4; j += 32) {
+        const float4 v = hr[j];
+        ss = fmaf(v.x, v.x, ss);
+        ss = fmaf(v.y, v.y, ss);
+        ss = fmaf(v.z, v.z, ss);
+        ss = fmaf(v.w, v.w, ss);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) s_rs[t] = 1.0f / sqrtf(ss / static_cast<float>(K) + nrm.eps);
+    }
+    __syncthreads();
+  }
   const int n0 = (blockIdx.x * kGemvWarps + warp) * kGemvRows;
   if (n0 >= N) return;
   const int nchunk = (K + 255) / 256;
@@ -228,11 +258,28 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
           const int n = min(n0 + r, N - 1);
           bf16x8_to_f32(ld_nc_v4(W + static_cast<size_t>(n) * K + k), w[r]);
         }
+        float gk[8];
+        if (nrm.xh != nullptr) {
+          const float4 g0 = *reinterpret_cast<const float4*>(nrm.g + k);
+          const float4 g1 = *reinterpret_cast<const float4*>(nrm.g + k + 4);
+          gk[0] = g0.x; gk[1] = g0.y; gk[2] = g0.z; gk[3] = g0.w;
+          gk[4] = g1.x; gk[5] = g1.y; gk[6] = g1.z; gk[7] = g1.w;
+        }
 #pragma unroll
         for (int t = 0; t < kGemvTok; ++t) {
           if (t < mt) {
             float xv[8];
-            bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(X + static_cast<size_t>(t0 + t) * K + k)), xv);
+            if (nrm.xh != nullptr) {
+              const float* hr = nrm.xh + static_cast<size_t>(t0 + t) * K + k;
+              const float4 h0 = *reinterpret_cast<const float4*>(hr);
+              const float4 h1 = *reinterpret_cast<const float4*>(hr + 4);
+              const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+              const float rs = s_rs[t0 + t];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) xv[j] = __bfloat162float(__float2bfloat16(hv[j] * rs * gk[j]));
+            } else {
+              bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(X + static_cast<size_t>(t0 + t) * K + k)), xv);
+            }
 #pragma unroll
             for (int r = 0; r < kGemvRows; ++r)
 #pragma unroll
@@ -418,17 +465,19 @@ size_t attention_smem_bytes(int, int hd) {
 // ---------------------------------------------------------------------------
 namespace {
 
-int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st) {
+int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
+                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
   const int rows_per_block = kGemvWarps * kGemvRows;
   return launch_pdl(gemv_kernel, dim3((N + rows_per_block - 1) / rows_per_block), dim3(kGemvWarps * 32), 0, st, W, X,
-                    M, N, K, e);
+                    M, N, K, e, nrm);
 }
 
 static int ablate_mask();
-int launch_gemm(Llama& m, const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st) {
+int launch_gemm(Llama& m, const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
+                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
   if (ablate_mask() & 4) return PEARL_OK;
   if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st);
-  return launch_gemv(W, X, M, N, K, e, st);
+  return launch_gemv(W, X, M, N, K, e, st, nrm);
 }
 
 // Diagnostics only (PEARL_ABLATE=attn|norm|gemm): skip a kernel class to
@@ -456,13 +505,15 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   const size_t layer_kv = static_cast<size_t>(c.max_seq) * nkv;
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
   const size_t attn_smem = attention_smem_bytes(M, hd);
+  // CUDA-core (draft) models fuse every RMSNorm into the consuming GEMV
+  const bool fuse_norm = c.gemm_kind == PEARL_GEMM_CUDACORE;
   for (int l = 0; l < c.n_layers; ++l) {
     const LayerW& L = m.layers[l];
-    if (!(abl & 2)) {
+    if (!(abl & 2) && !fuse_norm) {
       rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
       if (rc) return rc;
+      g_prof.mark(OP_NORM, st);
     }
-    g_prof.mark(OP_NORM, st);
     EpiArgs e{};
     e.kind = EPI_QKV;
     e.out_bf16 = m.q;
@@ -475,7 +526,8 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     e.n_q = nq;
     e.n_kv = nkv;
     e.hd = hd;
-    rc = launch_gemm(m, L.wqkv, m.x, M, nq + 2 * nkv, d, e, st);
+    rc = launch_gemm(m, L.wqkv, m.x, M, nq + 2 * nkv, d, e, st,
+                     fuse_norm ? GemvNorm{m.h, L.attn_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
     if (rc) return rc;
     g_prof.mark(OP_QKV, st);
     AttnArgs aa{m.q, e.kc, e.vc, m.o, pos, pos_add, M, H, KV, hd, scale};
@@ -496,16 +548,17 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
     if (rc) return rc;
     g_prof.mark(OP_O, st);
-    if (!(abl & 2)) {
+    if (!(abl & 2) && !fuse_norm) {
       rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
       if (rc) return rc;
+      g_prof.mark(OP_NORM, st);
     }
-    g_prof.mark(OP_NORM, st);
     EpiArgs g{};
     g.kind = EPI_SWIGLU;
     g.out_bf16 = m.act;
     g.ld = c.ffn;
-    rc = launch_gemm(m, L.wgu, m.x, M, 2 * c.ffn, d, g, st);
+    rc = launch_gemm(m, L.wgu, m.x, M, 2 * c.ffn, d, g, st,
+                     fuse_norm ? GemvNorm{m.h, L.mlp_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
     if (rc) return rc;
     g_prof.mark(OP_GU, st);
     rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r, st);
@@ -515,14 +568,19 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   if (!want_logits) return PEARL_OK;
   const int first = logits_all ? 0 : M - 1;
   const int rows = M - first;
-  rc = launch_pdl(rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, st, m.h, m.final_norm, m.x, d, c.norm_eps, first);
-  if (rc) return rc;
-  g_prof.mark(OP_NORM, st);
+  if (!fuse_norm) {
+    rc = launch_pdl(rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, st, m.h, m.final_norm, m.x, d, c.norm_eps,
+                    first);
+    if (rc) return rc;
+    g_prof.mark(OP_NORM, st);
+  }
   EpiArgs s{};
   s.kind = EPI_STORE_F32;
   s.out_f32 = logits;
   s.ld = c.vocab;
-  rc = launch_gemm(m, m.lm_head, m.x, rows, c.vocab, d, s, st);
+  rc = launch_gemm(m, m.lm_head, m.x, rows, c.vocab, d, s, st,
+                   fuse_norm ? GemvNorm{m.h + static_cast<size_t>(first) * d, m.final_norm, c.norm_eps}
+                             : GemvNorm{nullptr, nullptr, 0.f});
   g_prof.mark(OP_HEAD, st);
   return rc;
 }
@@ -543,6 +601,8 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   PEARL_ARG_CHECK(c.n_heads % c.n_kv_heads == 0, "n_heads % n_kv_heads");
   PEARL_ARG_CHECK(c.d_model % 8 == 0 && c.ffn % 8 == 0, "d_model and ffn must be multiples of 8");
   PEARL_ARG_CHECK(c.d_model <= 4 * kNormThreads * kNormVec, "d_model too large for the norm kernel");
+  PEARL_ARG_CHECK(c.gemm_kind != PEARL_GEMM_CUDACORE || (c.max_tokens <= kGemvMaxNormTok && c.d_model % 256 == 0),
+                  "CUDA-core models need max_tokens <= 64 and d_model % 256 == 0 (fused norm)");
   PEARL_ARG_CHECK(c.max_tokens >= 1 && c.max_tokens <= 64, "max_tokens in [1, 64]");
   PEARL_ARG_CHECK(c.max_seq >= 1 && c.max_seq <= 4096, "max_seq in [1, 4096]");
   Llama* m = new Llama();
