@@ -32,6 +32,18 @@ struct EpiArgs {
   int ld;           // leading dimension of out
 };
 
+// The per-element arithmetic, with explicit rounding (no FMA contraction), so
+// every call site -- GEMV, per-GEMM tcgen05 kernel, persistent forward --
+// produces the same bits whatever the compiler does around it.
+__device__ __forceinline__ float swiglu1(float gt, float up) {
+  return __fmul_rn(__fdiv_rn(gt, __fadd_rn(1.0f, expf(-gt))), up);
+}
+
+__device__ __forceinline__ void rope2(float x0, float x1, float c, float s, float* y0, float* y1) {
+  *y0 = __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, s));
+  *y1 = __fadd_rn(__fmul_rn(x0, s), __fmul_rn(x1, c));
+}
+
 // Handle four consecutive output rows n0..n0+3 (n0 % 4 == 0) for token t.
 __device__ __forceinline__ void epilogue4(const EpiArgs& e, int t, int n0, const float* v, int N) {
   switch (e.kind) {
@@ -46,9 +58,7 @@ __device__ __forceinline__ void epilogue4(const EpiArgs& e, int t, int n0, const
     case EPI_SWIGLU: {
       // rows (2j, 2j+1) = (gate_j, up_j)
       for (int r = 0; r < 4; r += 2) {
-        const float gt = v[r], up = v[r + 1];
-        const float s = gt / (1.0f + expf(-gt));
-        e.out_bf16[static_cast<size_t>(t) * e.ld + (n0 + r) / 2] = __float2bfloat16(s * up);
+        e.out_bf16[static_cast<size_t>(t) * e.ld + (n0 + r) / 2] = __float2bfloat16(swiglu1(v[r], v[r + 1]));
       }
       break;
     }
@@ -62,8 +72,7 @@ __device__ __forceinline__ void epilogue4(const EpiArgs& e, int t, int n0, const
           const int i = (n % e.hd) >> 1;  // rotation pair index within the head
           const float c = e.cos_t[static_cast<size_t>(p) * half + i];
           const float s = e.sin_t[static_cast<size_t>(p) * half + i];
-          w[r] = v[r] * c - v[r + 1] * s;
-          w[r + 1] = v[r] * s + v[r + 1] * c;
+          rope2(v[r], v[r + 1], c, s, &w[r], &w[r + 1]);
         }
         if (n0 < e.n_q) {
           for (int r = 0; r < 4; ++r) e.out_bf16[static_cast<size_t>(t) * e.n_q + n0 + r] = __float2bfloat16(w[r]);
@@ -81,5 +90,97 @@ __device__ __forceinline__ void epilogue4(const EpiArgs& e, int t, int n0, const
   }
 }
 
+// Epilogue of one 128-row output tile for tokens 0..M-1 on the tcgen05 paths
+// (per-GEMM kernel and persistent forward): E is the tile's fp32 result in
+// smem, E[row * ES + t]; 128 threads (et) take items (4-row group g, token
+// t) = (idx % 32, idx / 32), idx = et + 128 i.  Same arithmetic as epilogue4,
+// but every global load of all of a thread's items (residual rows, RoPE
+// tables, the position) is issued before any store, so a tile's epilogue
+// costs one memory round trip instead of one per item.
+template <int MAXI>
+__device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const float* E, int ES, int M, int N,
+                                              int et) {
+  constexpr int kGroups = 32;  // 128 rows / 4
+  const int nitems = kGroups * M;
+  switch (e.kind) {
+    case EPI_STORE_F32:
+#pragma unroll
+      for (int i = 0; i < MAXI; ++i) {
+        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        if (idx >= nitems || n0 >= N) continue;
+        float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
+        for (int r = 0; r < 4; ++r)
+          if (n0 + r < N) o[r] = E[(g * 4 + r) * ES + t];
+      }
+      break;
+    case EPI_RESID: {
+      float4 hv[MAXI];
+#pragma unroll
+      for (int i = 0; i < MAXI; ++i) {
+        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        if (idx < nitems && n0 + 3 < N)
+          hv[i] = *reinterpret_cast<const float4*>(e.out_f32 + static_cast<size_t>(t) * e.ld + n0);
+      }
+#pragma unroll
+      for (int i = 0; i < MAXI; ++i) {
+        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        if (idx >= nitems || n0 >= N) continue;
+        float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
+        if (n0 + 3 < N) {
+          *reinterpret_cast<float4*>(o) = make_float4(hv[i].x + E[(g * 4) * ES + t], hv[i].y + E[(g * 4 + 1) * ES + t],
+                                                      hv[i].z + E[(g * 4 + 2) * ES + t], hv[i].w + E[(g * 4 + 3) * ES + t]);
+        } else {
+          for (int r = 0; r < 4; ++r)
+            if (n0 + r < N) o[r] += E[(g * 4 + r) * ES + t];
+        }
+      }
+      break;
+    }
+    case EPI_SWIGLU:
+#pragma unroll
+      for (int i = 0; i < MAXI; ++i) {
+        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        if (idx >= nitems || n0 >= N) continue;
+        for (int r = 0; r < 4; r += 2)
+          e.out_bf16[static_cast<size_t>(t) * e.ld + (n0 + r) / 2] =
+              __float2bfloat16(swiglu1(E[(g * 4 + r) * ES + t], E[(g * 4 + r + 1) * ES + t]));
+      }
+      break;
+    case EPI_QKV: {
+      const int p0 = *e.pos + e.pos_add;
+      const int half = e.hd >> 1;
+      float2 cs[MAXI], sn[MAXI];
+#pragma unroll
+      for (int i = 0; i < MAXI; ++i) {
+        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        if (idx < nitems && n0 < e.n_q + e.n_kv) {
+          const size_t off = static_cast<size_t>(p0 + t) * half + ((n0 % e.hd) >> 1);
+          cs[i] = *reinterpret_cast<const float2*>(e.cos_t + off);
+          sn[i] = *reinterpret_cast<const float2*>(e.sin_t + off);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MAXI; ++i) {
+        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        if (idx >= nitems || n0 >= N) continue;
+        const int p = p0 + t;
+        float v[4];
+        for (int r = 0; r < 4; ++r) v[r] = E[(g * 4 + r) * ES + t];
+        if (n0 < e.n_q + e.n_kv) {
+          float w[4];
+          rope2(v[0], v[1], cs[i].x, sn[i].x, &w[0], &w[1]);
+          rope2(v[2], v[3], cs[i].y, sn[i].y, &w[2], &w[3]);
+          bf16* dst = n0 < e.n_q ? e.out_bf16 + static_cast<size_t>(t) * e.n_q + n0
+                                 : e.kc + static_cast<size_t>(p) * e.n_kv + (n0 - e.n_q);
+          for (int r = 0; r < 4; ++r) dst[r] = __float2bfloat16(w[r]);
+        } else {
+          bf16* dst = e.vc + static_cast<size_t>(p) * e.n_kv + (n0 - e.n_q - e.n_kv);
+          for (int r = 0; r < 4; ++r) dst[r] = __float2bfloat16(v[r]);
+        }
+      }
+      break;
+    }
+  }
+}
 
 }  // namespace pearl

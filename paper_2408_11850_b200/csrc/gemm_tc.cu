@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -194,41 +195,42 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         if (!*s_last) continue;
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         // Fixed split order => independent of arrival order and of M.  Each
-        // thread owns one row; per 4-token quad all S float4 loads are in
-        // flight together, then summed in split order.
+        // thread owns one row; loads of up to 16 (split, token-quad) float4
+        // are in flight together, then summed per quad in split order.
         const float* src = a.partials + (static_cast<size_t>(tile) * a.seg_max * kTileN + row) * Mp;
         const size_t sstride = static_cast<size_t>(kTileN) * Mp;
-        for (int q = 0; q < Mp / 4; ++q) {
-          float4 p[16];
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int s0 = 0; s0 < u.nseg; s0 += 16) {
+        constexpr int NQ = NT * 4;          // token quads per row (max)
+        constexpr int SB = 16 / NQ;         // splits per batch
+        const int nq = Mp / 4;
+        float4 acc[NQ];
 #pragma unroll
-            for (int s = 0; s < 16; ++s)
-              if (s0 + s < u.nseg) p[s] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + s) * sstride + 4 * q));
+        for (int q = 0; q < NQ; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s0 = 0; s0 < u.nseg; s0 += SB) {
+          float4 p[SB][NQ];
 #pragma unroll
-            for (int s = 0; s < 16; ++s)
-              if (s0 + s < u.nseg) {
-                acc.x += p[s].x;
-                acc.y += p[s].y;
-                acc.z += p[s].z;
-                acc.w += p[s].w;
+          for (int sb = 0; sb < SB; ++sb)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+              if (s0 + sb < u.nseg && q < nq)
+                p[sb][q] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + sb) * sstride + 4 * q));
+#pragma unroll
+          for (int sb = 0; sb < SB; ++sb)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+              if (s0 + sb < u.nseg && q < nq) {
+                acc[q].x += p[sb][q].x;
+                acc[q].y += p[sb][q].y;
+                acc[q].z += p[sb][q].z;
+                acc[q].w += p[sb][q].w;
               }
-          }
-          *reinterpret_cast<float4*>(E + row * ES + 4 * q) = acc;
         }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          if (q < nq) *reinterpret_cast<float4*>(E + row * ES + 4 * q) = acc[q];
         if (et == 0) a.flags[tile] = 0;
       }
       epi_bar();
-      const int groups = kTileN / 4;
-      for (int idx = et; idx < groups * a.M; idx += kEpiThreads) {
-        const int g = idx % groups, t = idx / groups;
-        const int n0 = tile * kTileN + g * 4;
-        if (n0 >= a.N) continue;
-        float w[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) w[r] = E[(g * 4 + r) * ES + t];
-        epilogue4(a.e, t, n0, w, a.N);
-      }
+      epilogue_tile<NT * 4>(a.e, tile, E, ES, a.M, a.N, et);
       epi_bar();
     }
   }
@@ -286,6 +288,10 @@ cudaError_t set_attr() {
 }
 
 }  // namespace
+
+int tc_encode_2d(CUtensorMap* map, const void* base, int inner, int rows, int box_rows) {
+  return encode_2d(map, base, inner, rows, box_rows);
+}
 
 // Split-K factor for an (N, K) weight: enough (tile, split) units to keep
 // every SM's pipeline busy while per-SM work stays balanced.  Depends on the

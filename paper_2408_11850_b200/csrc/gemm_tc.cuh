@@ -33,7 +33,8 @@ struct TcGemmCtx {
   int n_flags = 0;
   int max_tokens = 0;
   int num_sms = 148;
-  int min_plan_splits = 1;  // workspace sized for at least this many splits (microbenchmarks)
+  int min_plan_splits = 1;
+  int l2_prefetch_iters = 0;  // next-GEMM weight tiles per CTA requested into L2 (0: off)  // workspace sized for at least this many splits (microbenchmarks)
   // per weight matrix, keyed by (address, N, K): a map encodes the shape too
   std::map<std::tuple<const void*, int, int>, TcWeightMap> wmaps;
 };
@@ -46,5 +47,7 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
 int tc_splits(int N, int K, int num_sms);
 // most stream-K segments any tile of an (tiles x KB) GEMM is cut into over G CTAs
 int tc_seg_max(int tiles, int KB, int G);
+// bf16 [rows, inner] row-major tensor map, box kTileK x box_rows, 128B swizzle
+int tc_encode_2d(CUtensorMap* map, const void* base, int inner, int rows, int box_rows);
 
 }  // namespace pearl

@@ -33,6 +33,7 @@
 
 #include "common.h"
 #include "epilogue.cuh"
+#include "fwd_mega.cuh"
 #include "gemm_tc.cuh"
 
 namespace pearl {
@@ -64,6 +65,16 @@ struct Llama {
   bf16* o = nullptr;      // [T, H hd]
   bf16* act = nullptr;    // [T, ffn]
   TcGemmCtx tc;           // tcgen05 path state (split-K scratch, descriptors)
+  // persistent forward (fwd_mega.cu): phase lists per (window M, logits mode),
+  // built once at create time, device resident
+  bool mega_ok = false;
+  int mega_grid = 0;
+  MegaMap* mg_maps = nullptr;       // [4 L + 1 weight maps | 4 x 16 activation maps]
+  MegaPhase* mg_phases = nullptr;   // every list, concatenated
+  unsigned* mg_counter = nullptr;
+  unsigned long long* mg_trace = nullptr;  // set only inside pearl_llama_mega_trace
+  int mg_off[17][3] = {};           // list offset / length per (M, mode)
+  int mg_len[17][3] = {};
 };
 
 // Optional per-op timing of an eager forward (pearl_llama_profile): an event
@@ -117,15 +128,17 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens, const bf16* __r
   for (int i = threadIdx.x; i < d; i += blockDim.x) h[static_cast<size_t>(t) * d + i] = __bfloat162float(row[i]);
 }
 
-// x[t] = bf16(h[t] * rsqrt(mean(h[t]^2) + eps) * g); one block per token,
-// fixed reduction order.  The row is read once with all 16-byte loads in
-// flight (d <= 8192: at most 8 float4 per thread) and kept in registers.
-constexpr int kNormThreads = 256;
-constexpr int kNormVec = 8;
+// x[t] = bf16(h[t] * rsqrt(mean(h[t]^2) + eps) * g); one 128-thread block per
+// token.  Fixed order: thread-strided float4 sums in k order, warp xor tree,
+// (w0 + w1) + (w2 + w3) -- exactly mg_norm_row of the persistent forward
+// kernel, so both paths produce identical bits.
+constexpr int kNormThreads = 128;
+constexpr int kNormVec = 16;  // d <= 4 * 128 * 16 = 8192
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g,
                                                                bf16* __restrict__ x, int d, float eps, int row_off) {
   pdl_wait();
   pdl_trigger();
+  __shared__ float red[4];
   const int t = blockIdx.x + row_off;
   const float4* hr = reinterpret_cast<const float4*>(h + static_cast<size_t>(t) * d);
   const int nv = d / 4;
@@ -138,26 +151,21 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __re
   float ss = 0.f;
 #pragma unroll
   for (int i = 0; i < kNormVec; ++i) {
-    ss = fmaf(v[i].x, v[i].x, ss);
-    ss = fmaf(v[i].y, v[i].y, ss);
-    ss = fmaf(v[i].z, v[i].z, ss);
-    ss = fmaf(v[i].w, v[i].w, ss);
+    if (threadIdx.x + i * kNormThreads < nv) {
+      ss = fmaf(v[i].x, v[i].x, ss);
+      ss = fmaf(v[i].y, v[i].y, ss);
+      ss = fmaf(v[i].z, v[i].z, ss);
+      ss = fmaf(v[i].w, v[i].w, ss);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  __shared__ float ws[32];
-  __shared__ float s_rs;
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = ss;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float tot = 0.f;
-    for (int w = 0; w < kNormThreads / 32; ++w) tot += ws[w];
-    s_rs = 1.0f / sqrtf(tot / static_cast<float>(d) + eps);
-  }
-  __syncthreads();
-  const float rs = s_rs;
+  const float tot = (red[0] + red[1]) + (red[2] + red[3]);
+  const float rs = 1.0f / sqrtf(tot / static_cast<float>(d) + eps);
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  uint2* xr = reinterpret_cast<uint2*>(x + static_cast<size_t>(blockIdx.x) * d);
+  uint2* xr = reinterpret_cast<uint2*>(x + static_cast<size_t>(t) * d);
 #pragma unroll
   for (int i = 0; i < kNormVec; ++i) {
     const int j = threadIdx.x + i * kNormThreads;
@@ -305,20 +313,20 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
 
 // ---------------------------------------------------------------------------
 // K4: causal attention of the window's M queries over the KV cache.
-// One block per (query head h, group of <= 16 window tokens); its 8 warps take 32-position chunks of the
-// context round-robin (chunk c -> warp c % 8).  Within a warp lane j owns
+// One block per (query head h, window token); its 4 warps take 32-position chunks of the
+// context round-robin (chunk c -> warp c % 4).  Within a warp lane j owns
 // position c*32+j: it computes the full fixed-order q.k dot product for every
 // window token, the warp reduces max / sum-of-exp with shuffles, and the
 // exp-weighted V sum is accumulated with lanes over head dims.  Each warp
 // keeps a running (max, sum, o) per token over its chunks (online softmax in
-// chunk order); the block then merges the 8 warps' states in warp order.
+// chunk order); the block then merges the 4 warps' states in warp order.
 // Every step depends only on the token's own position and the cache, never
 // on how many tokens share the launch (batch invariance), and there is no
 // inter-block communication.
 // ---------------------------------------------------------------------------
-constexpr int kAttnWarps = 8;
+constexpr int kAttnWarps = 4;  // == the persistent kernel's epilogue warps (identical arithmetic)
 constexpr int kAttnLanesPos = 32;  // positions per warp chunk
-constexpr int kAttnTokens = 1;     // window tokens per block (grid.y = ceil(M / kAttnTokens))
+constexpr int kAttnMaxTokens = 16; // window tokens per block: AttnArgs::tpb <= this
 
 struct AttnArgs {
   const bf16* q;      // [M, H, hd]
@@ -327,6 +335,7 @@ struct AttnArgs {
   bf16* o;            // [M, H, hd]
   const int32_t* pos;
   int pos_add, M, H, KV, hd;
+  int tpb;            // window tokens per block (shares each K/V chunk load; no effect on the arithmetic)
   float scale;
 };
 
@@ -337,8 +346,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs 
   pdl_wait();
   pdl_trigger();
   const int h = blockIdx.x;
-  const int t0 = blockIdx.y * kAttnTokens;            // first window token of this block
-  const int MT = min(kAttnTokens, a.M - t0);          // tokens handled here
+  const int t0 = blockIdx.y * a.tpb;                  // first window token of this block
+  const int MT = min(a.tpb, a.M - t0);                // tokens handled here
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p0 = *a.pos + a.pos_add + t0;             // position of the block's first token
   const int ctx_max = p0 + MT;
@@ -348,8 +357,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs 
   // per-warp state [M][HD + 2] in smem: o (HD), m, l
   float* st_all = reinterpret_cast<float*>(attn_smem);
   float* st = st_all + static_cast<size_t>(warp) * MT * (HD + 2);
-  bf16* Qs = reinterpret_cast<bf16*>(st_all + static_cast<size_t>(kAttnWarps) * kAttnTokens * (HD + 2));  // [MT][HD]
-  bf16* Vw = Qs + kAttnTokens * HD + static_cast<size_t>(warp) * kAttnLanesPos * HD;  // this warp's V chunk
+  bf16* Qs = reinterpret_cast<bf16*>(st_all + static_cast<size_t>(kAttnWarps) * a.tpb * (HD + 2));  // [MT][HD]
+  bf16* Vw = Qs + a.tpb * HD + static_cast<size_t>(warp) * kAttnLanesPos * HD;  // this warp's V chunk
   for (int i = threadIdx.x; i < MT * HD / 8; i += blockDim.x) {
     const int t = i / (HD / 8), v = i % (HD / 8);
     reinterpret_cast<uint4*>(Qs + t * HD)[v] =
@@ -360,17 +369,23 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs 
   for (int c = warp; c < n_chunks; c += kAttnWarps) {
     const int j = c * kAttnLanesPos + lane;  // this lane's position
     const bool have = j < ctx_max;
-    // K row of position j into registers (16-byte loads, all in flight)
-    uint4 kr[HD / 8];
+    // K row of position j and the chunk's V rows (flat 16-byte pieces
+    // lane + 32 k) into registers, all loads in flight; V then to smem
+    uint4 kr[HD / 8], vr[HD / 8];
 #pragma unroll
     for (int v = 0; v < HD / 8; ++v)
       kr[v] = have ? *reinterpret_cast<const uint4*>(a.kc + j * kstride + kvh * HD + v * 8) : make_uint4(0, 0, 0, 0);
-    // stage the chunk's V rows once (coalesced 16-byte loads), reused by every token
-    for (int i = lane; i < kAttnLanesPos * HD / 8; i += 32) {
-      const int jj = i / (HD / 8), v = i % (HD / 8);
-      const int jp = c * kAttnLanesPos + jj;
-      reinterpret_cast<uint4*>(Vw + jj * HD)[v] =
-          jp < ctx_max ? *reinterpret_cast<const uint4*>(a.vc + jp * kstride + kvh * HD + v * 8) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < HD / 8; ++k) {
+      const int i = lane + 32 * k;
+      const int jp = c * kAttnLanesPos + i / (HD / 8);
+      vr[k] = jp < ctx_max ? *reinterpret_cast<const uint4*>(a.vc + jp * kstride + kvh * HD + (i % (HD / 8)) * 8)
+                           : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < HD / 8; ++k) {
+      const int i = lane + 32 * k;
+      reinterpret_cast<uint4*>(Vw + (i / (HD / 8)) * HD)[i % (HD / 8)] = vr[k];
     }
     __syncwarp();
     for (int t = 0; t < MT; ++t) {
@@ -455,8 +470,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs 
   }
 }
 
-size_t attention_smem_bytes(int, int hd) {
-  return static_cast<size_t>(kAttnWarps) * kAttnTokens * (hd + 2) * 4 + static_cast<size_t>(kAttnTokens) * hd * 2 +
+size_t attention_smem_bytes(int tpb, int hd) {
+  return static_cast<size_t>(kAttnWarps) * tpb * (hd + 2) * 4 + static_cast<size_t>(tpb) * hd * 2 +
          static_cast<size_t>(kAttnWarps) * kAttnLanesPos * hd * 2 + 64;
 }
 
@@ -464,6 +479,15 @@ size_t attention_smem_bytes(int, int hd) {
 // host side
 // ---------------------------------------------------------------------------
 namespace {
+
+int attention_tpb(int M, int H) {
+  static const int forced = [] {
+    const char* v = std::getenv("PEARL_ATTN_TPB");
+    return v ? std::atoi(v) : 0;
+  }();
+  int t = forced > 0 ? forced : (M * H + 295) / 296;  // ~2 blocks per SM (measured best, llama2-7b)
+  return std::max(1, std::min({t, kAttnMaxTokens, M}));
+}
 
 int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
                 GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
@@ -493,18 +517,72 @@ static int ablate_mask() {
   return m;
 }
 
+// The persistent forward serves a call when PEARL_FWD_PERSISTENT is set, or
+// for every eligible call with PEARL_MEGA=1.  Off by default: on B200 its
+// software phase barriers cost more than the per-op kernels' launch gaps
+// with programmatic dependent launch ("persistent forward").
+static bool mega_default() {
+  static const bool on = [] {
+    const char* v = std::getenv("PEARL_MEGA");
+    return v != nullptr && std::string(v) == "1";
+  }();
+  return on;
+}
+
+// Experiment bits of the persistent kernel (PEARL_MEGA_OPTS).
+static int mega_opts() {
+  static const int o = [] {
+    const char* v = std::getenv("PEARL_MEGA_OPTS");
+    return v ? std::atoi(v) : 0;
+  }();
+  return o;
+}
+
+// Diagnostics only (PEARL_STOP=k): run only the first k ops / phases of a
+// forward (embed, then per layer norm, qkv, attn, o, norm, gate_up, down,
+// then final norm, lm_head), so both paths' intermediate buffers can be
+// compared (pearl_llama_debug_buffer).
+static int stop_after() {
+  const char* v = std::getenv("PEARL_STOP");
+  return v ? std::atoi(v) : -1;
+}
+
 int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_add, bool logits_all,
-                  bool want_logits, float* logits, cudaStream_t st) {
+                  bool want_logits, float* logits, cudaStream_t st, bool use_mega) {
   const int abl = ablate_mask();
+  const int stop = stop_after();
+  int n_ops = 0;
+  auto halt = [&]() { return stop >= 0 && ++n_ops >= stop; };
+  if (m.mega_ok && use_mega && !abl && !g_prof.on && M <= kMegaMaxTokens) {
+    const int mode = !want_logits ? 0 : (logits_all ? 2 : 1);
+    MegaArgs A{};
+    A.phases = m.mg_phases + m.mg_off[M][mode];
+    A.n_phases = stop >= 0 ? std::min(stop, m.mg_len[M][mode]) : m.mg_len[M][mode];
+    A.maps = m.mg_maps;
+    A.partials = m.tc.partials;
+    A.tile_flags = m.tc.tile_flags;
+    A.counter = m.mg_counter;
+    A.tokens = tokens;
+    A.pos = pos;
+    A.pos_add = pos_add;
+    A.logits = logits;
+    A.trace = m.mg_trace;
+    A.opts = mega_opts();
+    return mega_launch(A, m.mega_grid, st);
+  }
   const auto& c = m.cfg;
   const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads;
   const int nq = H * hd, nkv = KV * hd;
   int rc = launch_pdl(embed_kernel, dim3(M), dim3(256), 0, st, tokens, m.embed, m.h, d, c.vocab);
   if (rc) return rc;
   g_prof.mark(OP_EMBED, st);
+  if (halt()) return PEARL_OK;
   const size_t layer_kv = static_cast<size_t>(c.max_seq) * nkv;
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
-  const size_t attn_smem = attention_smem_bytes(M, hd);
+  // tokens per attention block: ~2 blocks per SM, each
+  // K/V chunk load shared by the block's tokens (PEARL_ATTN_TPB overrides)
+  const int tpb = attention_tpb(M, H);
+  const size_t attn_smem = attention_smem_bytes(tpb, hd);
   // CUDA-core (draft) models fuse every RMSNorm into the consuming GEMV
   const bool fuse_norm = c.gemm_kind == PEARL_GEMM_CUDACORE;
   for (int l = 0; l < c.n_layers; ++l) {
@@ -513,6 +591,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
       rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.attn_norm, m.x, d, c.norm_eps, 0);
       if (rc) return rc;
       g_prof.mark(OP_NORM, st);
+  if (halt()) return PEARL_OK;
     }
     EpiArgs e{};
     e.kind = EPI_QKV;
@@ -530,17 +609,19 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
                      fuse_norm ? GemvNorm{m.h, L.attn_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
     if (rc) return rc;
     g_prof.mark(OP_QKV, st);
-    AttnArgs aa{m.q, e.kc, e.vc, m.o, pos, pos_add, M, H, KV, hd, scale};
+  if (halt()) return PEARL_OK;
+    AttnArgs aa{m.q, e.kc, e.vc, m.o, pos, pos_add, M, H, KV, hd, tpb, scale};
     if (abl & 1)
       rc = PEARL_OK;
     else if (hd == 128)
-      rc = launch_pdl(attention_kernel<128>, dim3(H, (M + kAttnTokens - 1) / kAttnTokens), dim3(kAttnWarps * 32),
+      rc = launch_pdl(attention_kernel<128>, dim3(H, (M + tpb - 1) / tpb), dim3(kAttnWarps * 32),
                       attn_smem, st, aa);
     else
-      rc = launch_pdl(attention_kernel<64>, dim3(H, (M + kAttnTokens - 1) / kAttnTokens), dim3(kAttnWarps * 32),
+      rc = launch_pdl(attention_kernel<64>, dim3(H, (M + tpb - 1) / tpb), dim3(kAttnWarps * 32),
                       attn_smem, st, aa);
     if (rc) return rc;
     g_prof.mark(OP_ATTN, st);
+  if (halt()) return PEARL_OK;
     EpiArgs r{};
     r.kind = EPI_RESID;
     r.out_f32 = m.h;
@@ -548,10 +629,12 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
     if (rc) return rc;
     g_prof.mark(OP_O, st);
+  if (halt()) return PEARL_OK;
     if (!(abl & 2) && !fuse_norm) {
       rc = launch_pdl(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, m.h, L.mlp_norm, m.x, d, c.norm_eps, 0);
       if (rc) return rc;
       g_prof.mark(OP_NORM, st);
+  if (halt()) return PEARL_OK;
     }
     EpiArgs g{};
     g.kind = EPI_SWIGLU;
@@ -561,9 +644,11 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
                      fuse_norm ? GemvNorm{m.h, L.mlp_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
     if (rc) return rc;
     g_prof.mark(OP_GU, st);
+  if (halt()) return PEARL_OK;
     rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r, st);
     if (rc) return rc;
     g_prof.mark(OP_DOWN, st);
+  if (halt()) return PEARL_OK;
   }
   if (!want_logits) return PEARL_OK;
   const int first = logits_all ? 0 : M - 1;
@@ -573,12 +658,13 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
                     first);
     if (rc) return rc;
     g_prof.mark(OP_NORM, st);
+  if (halt()) return PEARL_OK;
   }
   EpiArgs s{};
   s.kind = EPI_STORE_F32;
   s.out_f32 = logits;
   s.ld = c.vocab;
-  rc = launch_gemm(m, m.lm_head, m.x, rows, c.vocab, d, s, st,
+  rc = launch_gemm(m, m.lm_head, fuse_norm ? m.x : m.x + static_cast<size_t>(first) * d, rows, c.vocab, d, s, st,
                    fuse_norm ? GemvNorm{m.h + static_cast<size_t>(first) * d, m.final_norm, c.norm_eps}
                              : GemvNorm{nullptr, nullptr, 0.f});
   g_prof.mark(OP_HEAD, st);
@@ -587,6 +673,160 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
 
 std::once_flag g_attn_once;
 cudaError_t g_attn_err = cudaSuccess;
+
+// Phase lists of the persistent forward for every window size M <= 16 and
+// logits mode (0 none, 1 last row, 2 all rows), mirroring forward_chunk op
+// for op: same weights, same epilogues, same stream-K grid (num_sms), so the
+// two paths produce identical bits.
+int build_mega_plans(Llama& m) {
+  const auto& c = m.cfg;
+  if (c.gemm_kind != PEARL_GEMM_TCGEN05) return PEARL_OK;
+  int per_sm = 0;
+  PEARL_CUDA_TRY(mega_prepare());
+  PEARL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mega_kernel_ptr(), mega_threads(),
+                                                               mega_smem_bytes()));
+  if (per_sm < 1) return PEARL_OK;
+  const int G = m.tc.num_sms;
+  const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads, L = c.n_layers;
+  const int nq = H * hd, nkv = KV * hd;
+  const size_t layer_kv = static_cast<size_t>(c.max_seq) * nkv;
+  const int n_w = 4 * L + 1;
+  const int Mmax = std::min(kMegaMaxTokens, c.max_tokens);
+  std::vector<MegaMap> maps(static_cast<size_t>(n_w) + 4 * 16);
+  const int wq[5][2] = {{nq + 2 * nkv, d}, {d, nq}, {2 * c.ffn, d}, {d, c.ffn}, {c.vocab, d}};
+  for (int l = 0; l < L; ++l) {
+    const LayerW& Lw = m.layers[l];
+    const bf16* ws[4] = {Lw.wqkv, Lw.wo, Lw.wgu, Lw.wdown};
+    for (int k = 0; k < 4; ++k) {
+      int rc = tc_encode_2d(&maps[4 * l + k].map, ws[k], wq[k][1], wq[k][0], kMegaTileN);
+      if (rc) return rc;
+    }
+  }
+  int rc = tc_encode_2d(&maps[4 * L].map, m.lm_head, d, c.vocab, kMegaTileN);
+  if (rc) return rc;
+  auto xmap = [&](int M, int k) { return n_w + 4 * (M - 1) + k; };  // k: 0 x, 1 o, 2 act, 3 x last row
+  for (int M = 1; M <= Mmax; ++M) {
+    if ((rc = tc_encode_2d(&maps[xmap(M, 0)].map, m.x, d, M, kMegaMaxTokens))) return rc;
+    if ((rc = tc_encode_2d(&maps[xmap(M, 1)].map, m.o, nq, M, kMegaMaxTokens))) return rc;
+    if ((rc = tc_encode_2d(&maps[xmap(M, 2)].map, m.act, c.ffn, M, kMegaMaxTokens))) return rc;
+    if ((rc = tc_encode_2d(&maps[xmap(M, 3)].map, m.x + static_cast<size_t>(M - 1) * d, d, 1, kMegaMaxTokens)))
+      return rc;
+  }
+  std::vector<MegaPhase> all;
+  auto gemm = [&](int M, int wmap, int xm, int N, int K, const EpiArgs& e) {
+    MegaPhase p{};
+    p.kind = MG_GEMM;
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.KB = (K + kMegaTileK - 1) / kMegaTileK;
+    const int tiles = (N + kMegaTileN - 1) / kMegaTileN;
+    p.T = static_cast<long long>(tiles) * p.KB;
+    p.seg_max = tc_seg_max(tiles, p.KB, static_cast<int>(std::min<long long>(G, p.T)));
+    p.map_w = wmap;
+    p.map_x = xm;
+    p.e = e;
+    all.push_back(p);
+  };
+  auto norm = [&](int M, const float* gain, int row0) {
+    MegaPhase p{};
+    p.kind = MG_NORM;
+    p.M = M;
+    p.h = m.h;
+    p.gain = gain;
+    p.xout = m.x;
+    p.d = d;
+    p.row0 = row0;
+    p.eps = c.norm_eps;
+    all.push_back(p);
+  };
+  const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+  for (int M = 1; M <= Mmax; ++M) {
+    for (int mode = 0; mode < 3; ++mode) {
+      m.mg_off[M][mode] = static_cast<int>(all.size());
+      MegaPhase pe{};
+      pe.kind = MG_EMBED;
+      pe.M = M;
+      pe.h = m.h;
+      pe.d = d;
+      pe.embed = m.embed;
+      pe.V = c.vocab;
+      all.push_back(pe);
+      for (int l = 0; l < L; ++l) {
+        const LayerW& Lw = m.layers[l];
+        norm(M, Lw.attn_norm, 0);
+        EpiArgs e{};
+        e.kind = EPI_QKV;
+        e.out_bf16 = m.q;
+        e.kc = m.kcache + l * layer_kv;
+        e.vc = m.vcache + l * layer_kv;
+        e.cos_t = m.rope_cos;
+        e.sin_t = m.rope_sin;
+        e.n_q = nq;
+        e.n_kv = nkv;
+        e.hd = hd;
+        gemm(M, 4 * l + 0, xmap(M, 0), nq + 2 * nkv, d, e);
+        all.back().e_uses_pos = 1;
+        MegaPhase pa{};
+        pa.kind = MG_ATTN;
+        pa.M = M;
+        pa.q = m.q;
+        pa.kc = e.kc;
+        pa.vc = e.vc;
+        pa.o = m.o;
+        pa.H = H;
+        pa.KV = KV;
+        pa.hd = hd;
+        pa.scale = scale;
+        all.push_back(pa);
+        EpiArgs r{};
+        r.kind = EPI_RESID;
+        r.out_f32 = m.h;
+        r.ld = d;
+        gemm(M, 4 * l + 1, xmap(M, 1), d, nq, r);
+        norm(M, Lw.mlp_norm, 0);
+        EpiArgs g{};
+        g.kind = EPI_SWIGLU;
+        g.out_bf16 = m.act;
+        g.ld = c.ffn;
+        gemm(M, 4 * l + 2, xmap(M, 0), 2 * c.ffn, d, g);
+        gemm(M, 4 * l + 3, xmap(M, 2), d, c.ffn, r);
+      }
+      if (mode > 0) {
+        const int first = mode == 2 ? 0 : M - 1;
+        norm(M, m.final_norm, first);
+        EpiArgs s{};
+        s.kind = EPI_STORE_F32;
+        s.ld = c.vocab;
+        gemm(M - first, 4 * L, mode == 2 ? xmap(M, 0) : xmap(M, 3), c.vocab, d, s);
+        all.back().e_is_logits = 1;
+      }
+      m.mg_len[M][mode] = static_cast<int>(all.size()) - m.mg_off[M][mode];
+    }
+  }
+  for (const MegaPhase& p : all)
+    if (p.kind == MG_GEMM) {
+      const int tiles = static_cast<int>(p.T / p.KB);
+      if (static_cast<size_t>(tiles) * p.seg_max * kMegaTileN * kMegaPartialTok > m.tc.partial_floats ||
+          tiles > m.tc.n_flags) {
+        set_error("persistent forward: shape exceeds the planned split-K workspace");
+        return PEARL_ERR_ARG;
+      }
+    }
+  PEARL_CUDA_TRY(cudaMalloc(&m.mg_maps, maps.size() * sizeof(MegaMap)));
+  PEARL_CUDA_TRY(cudaMemcpy(m.mg_maps, maps.data(), maps.size() * sizeof(MegaMap), cudaMemcpyHostToDevice));
+  PEARL_CUDA_TRY(cudaMalloc(&m.mg_phases, all.size() * sizeof(MegaPhase)));
+  PEARL_CUDA_TRY(cudaMemcpy(m.mg_phases, all.data(), all.size() * sizeof(MegaPhase), cudaMemcpyHostToDevice));
+  int max_len = 0;
+  for (int M = 1; M <= Mmax; ++M)
+    for (int mode = 0; mode < 3; ++mode) max_len = std::max(max_len, m.mg_len[M][mode]);
+  const size_t ctr_bytes = static_cast<size_t>(max_len) * kMegaCtrStride * sizeof(unsigned);
+  PEARL_CUDA_TRY(cudaMalloc(&m.mg_counter, ctr_bytes));
+  PEARL_CUDA_TRY(cudaMemset(m.mg_counter, 0, ctr_bytes));
+  m.mega_grid = G;
+  m.mega_ok = true;
+  return PEARL_OK;
+}
 
 }  // namespace
 }  // namespace pearl
@@ -635,14 +875,15 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   if ((e = cudaMalloc(&m->act, T * c.ffn * sizeof(bf16)))) return fail(e);
   std::call_once(g_attn_once, [] {
     g_attn_err = cudaFuncSetAttribute(attention_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(attention_smem_bytes(64, 128)));
+                                      static_cast<int>(attention_smem_bytes(kAttnMaxTokens, 128)));
     if (g_attn_err == cudaSuccess)
       g_attn_err = cudaFuncSetAttribute(attention_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(attention_smem_bytes(64, 64)));
+                                        static_cast<int>(attention_smem_bytes(kAttnMaxTokens, 64)));
   });
   if (g_attn_err) return fail(g_attn_err);
   if (c.gemm_kind == PEARL_GEMM_TCGEN05) {
     int rc = tc_init(m->tc, c);
+    if (!rc) rc = build_mega_plans(*m);
     if (rc) {
       delete m;
       return rc;
@@ -661,6 +902,9 @@ extern "C" int pearl_llama_destroy(void* handle) {
   cudaFree(m->o);
   cudaFree(m->act);
   tc_free(m->tc);
+  if (m->mg_maps) cudaFree(m->mg_maps);
+  if (m->mg_phases) cudaFree(m->mg_phases);
+  if (m->mg_counter) cudaFree(m->mg_counter);
   delete m;
   return PEARL_OK;
 }
@@ -722,7 +966,8 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
   for (int c0 = 0; c0 < n_tokens; c0 += T) {
     const int mt = std::min(T, n_tokens - c0);
     const bool last_chunk = c0 + mt == n_tokens;
-    int rc = forward_chunk(*m, tokens + c0, mt, pos, c0, !last_only, last_chunk && logits != nullptr, logits, st);
+    int rc = forward_chunk(*m, tokens + c0, mt, pos, c0, !last_only, last_chunk && logits != nullptr, logits, st,
+                           (flags & PEARL_FWD_PERSISTENT) != 0 || mega_default());
     if (rc) return rc;
   }
   if (flags & PEARL_FWD_ADVANCE) {
@@ -730,6 +975,59 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
     if (rc) return rc;
   }
   return PEARL_OK;
+}
+
+// Diagnostic: copy an internal activation buffer (0 h fp32 [T, d], 1 x, 2 q,
+// 3 o, 4 act; bf16) to dst.
+extern "C" int pearl_llama_debug_buffer(void* handle, int which, void* dst, size_t bytes, void* stream) {
+  Llama* m = static_cast<Llama*>(handle);
+  PEARL_ARG_CHECK(m && dst && which >= 0 && which <= 6, "bad debug_buffer arguments");
+  const void* src[7] = {m->h, m->x, m->q, m->o, m->act, m->tc.tile_flags, m->mg_counter};
+  PEARL_CUDA_TRY(cudaMemcpyAsync(dst, src[which], bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return PEARL_OK;
+}
+
+// Diagnostic: one persistent-kernel forward with per-CTA phase timestamps.
+// out[3p + 0] = phase kind, out[3p + 1] = us until the last CTA finished
+// phase p, out[3p + 2] = us until the first CTA finished it (both from the
+// earliest CTA start).  Returns the phase count (or a negative error).
+extern "C" int pearl_llama_mega_trace(void* handle, const int32_t* tokens, int n_tokens, int32_t* pos, int flags,
+                                      float* logits, float* out, int max_phases, void* stream) {
+  Llama* m = static_cast<Llama*>(handle);
+  PEARL_ARG_CHECK(m && tokens && pos && out && n_tokens >= 1, "bad trace arguments");
+  PEARL_ARG_CHECK(m->mega_ok && n_tokens <= std::min(kMegaMaxTokens, m->cfg.max_tokens), "persistent forward not used");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int mode = logits == nullptr ? 0 : ((flags & PEARL_FWD_LAST_LOGITS) ? 1 : 2);
+  const int np = m->mg_len[n_tokens][mode];
+  const int G = m->mega_grid;
+  PEARL_ARG_CHECK(np <= max_phases, "max_phases too small");
+  const size_t n = static_cast<size_t>(np + 1) * G;
+  PEARL_CUDA_TRY(cudaStreamSynchronize(st));
+  PEARL_CUDA_TRY(cudaMalloc(&m->mg_trace, n * sizeof(unsigned long long)));
+  int rc = forward_chunk(*m, tokens, n_tokens, pos, 0, mode == 2, mode != 0, logits, st, true);
+  std::vector<unsigned long long> h(n);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaMemcpy(h.data(), m->mg_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaFree(m->mg_trace);
+  m->mg_trace = nullptr;
+  if (rc) return rc;
+  PEARL_CUDA_TRY(e);
+  std::vector<MegaPhase> ph(np);
+  PEARL_CUDA_TRY(cudaMemcpy(ph.data(), m->mg_phases + m->mg_off[n_tokens][mode], np * sizeof(MegaPhase),
+                            cudaMemcpyDeviceToHost));
+  unsigned long long t0 = ~0ull;
+  for (int b = 0; b < G; ++b) t0 = std::min(t0, h[static_cast<size_t>(np) * G + b]);
+  for (int p = 0; p < np; ++p) {
+    unsigned long long lo = ~0ull, hi = 0;
+    for (int b = 0; b < G; ++b) {
+      lo = std::min(lo, h[static_cast<size_t>(p) * G + b]);
+      hi = std::max(hi, h[static_cast<size_t>(p) * G + b]);
+    }
+    out[3 * p] = static_cast<float>(ph[p].kind);
+    out[3 * p + 1] = static_cast<float>(hi - t0) * 1e-3f;
+    out[3 * p + 2] = static_cast<float>(lo - t0) * 1e-3f;
+  }
+  return np;
 }
 
 // Per-op device time (ms) of one eager forward: out[op] for op in

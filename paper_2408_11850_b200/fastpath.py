@@ -215,7 +215,6 @@ class PairRuntime:
     def graph(self, key: tuple, body) -> torch.cuda.CUDAGraph:
         g = self.graphs.get(key)
         if g is None:
-            # warm up once eagerly on a side stream (cudaFuncSetAttribute etc.), then capture
             g = torch.cuda.CUDAGraph()
             c0 = int(self.lib.pearl_launch_count())
             with torch.cuda.graph(g):
@@ -338,6 +337,7 @@ class _GammaPlanner:
         self.gmax = gamma_max
         self.acc, self.exam = 3.0, 4.0  # prior alpha 0.75
         self.gamma = gamma0
+        self.started = False
 
     def _t_target(self, m: int) -> float:
         ks = sorted(self.t_t)
@@ -353,16 +353,30 @@ class _GammaPlanner:
         self.acc += accepted
         self.exam += accepted + rejected
 
+    def candidates(self) -> List[int]:
+        return [g for g in self.GRID if g <= self.gmax]
+
+    def neighbors(self, g: int) -> List[int]:
+        """Draft lengths reachable from g in one decision (itself and the grid neighbours)."""
+        c = self.candidates()
+        if g not in c:
+            return c
+        i = c.index(g)
+        return c[max(0, i - 1):i + 2]
+
     def next_gamma(self) -> int:
+        """First call: the best grid value; afterwards at most one grid step
+        per decision (hysteresis), which also bounds the set of step graphs a
+        decode can need (precaptured by decode_pearl)."""
         alpha = self.acc / self.exam
         best, best_rate = 1, -1.0
-        for g in self.GRID:
-            if g > self.gmax:
-                break
+        cands = self.candidates() if not self.started else self.neighbors(self.gamma)
+        for g in cands:
             rate = pearl_tokens_per_step(alpha, g) / max(self._t_target(g), g * self.t_d)
             if rate > best_rate:
                 best, best_rate = g, rate
         self.gamma = best
+        self.started = True
         return best
 
 
@@ -392,6 +406,7 @@ def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], c
     tab_d = _Tables(rt, rt.u_draft, None if cfg.greedy else root.split(0), S_DCUR)
     tab_v = _Tables(rt, rt.u_verify, None if cfg.greedy else root.split(1), S_VCUR)
     invt = inv_temp(cfg.temperature)
+    _precapture_pearl(rt, planner, gamma, invt, bool(cfg.greedy), bool(concurrent))
     committed: List[int] = list(seq0)
     pending: List[int] = []
     dpos = n0 - 1
@@ -438,6 +453,20 @@ def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], c
         steps.append(trace)
         produced = len(committed) - n0
     return DecodeResult(tuple(committed[n0:]), tuple(steps), stats=stats)
+
+
+def _precapture_pearl(rt: PairRuntime, planner, gamma: int, invt: float, greedy: bool, concurrent: bool) -> None:
+    """Capture every step graph this decode can reach before it starts: keys
+    (pending k, gamma, draft catch-up m0 = 1) with k = 0 (pre-verify) or
+    k = gamma' - 1 for each gamma' one planner decision away (post-verify).
+    Graph capture (~tens of ms each) then never lands inside a decode; rarer
+    keys (m0 > 1) are still captured on first use."""
+    gammas = planner.candidates() if planner is not None else [gamma]
+    for g in gammas:
+        prevs = planner.neighbors(g) if planner is not None else [g]
+        for k in sorted({0} | {gp - 1 for gp in prevs if gp > 1}):
+            key = ("pearl", k, g, 1, greedy, invt, concurrent)
+            rt.graph(key, lambda k=k, g=g: rt._pearl_body(k, g, 1, invt, greedy, concurrent))
 
 
 def steps_mode_post(steps) -> bool:
