@@ -108,6 +108,10 @@ def _prompts(n, P, V, seed):
     return [rng.integers(2, V, P).tolist() for _ in range(n)]
 
 
+# alignment knob per pair, calibrated on B200 to alpha-hat ~0.9 at T=1 (tools/calib_alpha.py)
+PAIR_BRANCH_STD = {"llama2-7b/68m": 5e-4, "dsc-33b/1.3b": 1.7e-4, "llama3-70b/8b": 8e-5, "tiny": 2e-4}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -119,7 +123,8 @@ def run_gpu(args):
     import paper_2408_11850_b200 as pk
     from paper_2408_11850_b200 import _lib, llama
 
-    align = llama.AlignSpec(branch_std=args.branch_std, kappa=args.kappa)
+    align = llama.AlignSpec(branch_std=args.branch_std if args.branch_std is not None else PAIR_BRANCH_STD[args.pair],
+                            kappa=args.kappa)
     target, draft = llama.build_pair(args.pair, gemm_target=args.gemm_target, align=align,
                                      max_seq=args.prompt + args.new + 2 * args.gamma_max + 16, max_tokens=64,
                                      temperature=1.0 if args.temperature <= 0 else args.temperature)
@@ -389,7 +394,8 @@ def main():
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--new", type=int, default=128)
     ap.add_argument("--temperature", type=float, default=1.0)
-    ap.add_argument("--branch-std", type=float, default=5e-4)
+    ap.add_argument("--branch-std", type=float, default=None,
+                    help="alignment knob (default per pair, calibrated to alpha-hat ~0.9 at T=1: tools/calib_alpha.py)")
     ap.add_argument("--kappa", type=float, default=13.0)
     ap.add_argument("--gemm-target", default="tcgen05")
     ap.add_argument("--cpu-new", type=int, default=16)

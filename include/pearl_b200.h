@@ -140,7 +140,8 @@ typedef struct {
   int32_t max_tokens; /* largest window processed in one pass (chunking) */
   int32_t gemm_kind;  /* PEARL_GEMM_*                                    */
   float norm_eps;
-  float reserved;
+  int32_t sm_count;  /* SMs the model's stream-K grids span (0: all);  \
+                        must match the partition it runs on            */
 } pearl_llama_config;
 
 /* Weight / cache pointer table, in this order (all device pointers):
@@ -175,6 +176,22 @@ int pearl_llama_forward(void* handle, const int32_t* tokens, int n_tokens, int32
                         int flags, float* logits, void* stream);
 
 size_t pearl_llama_workspace_bytes(void* handle, int n_tokens);
+
+/* Keep [base, base + bytes) -- a model's packed streamed weights -- in
+ * persisting L2 lines: every kernel of the model's forwards carries an L2
+ * access-policy window over it (hit ratio = granted / bytes).  For a draft
+ * model this serves its per-token weight reads from L2 instead of HBM,
+ * which the concurrently running target saturates.  *granted (optional) =
+ * the device's persisting-L2 size after the call; bytes = 0 clears it. */
+int pearl_llama_set_l2_window(void* handle, const void* base, size_t bytes, size_t* granted);
+
+/* SM partition for two concurrently running models (green contexts):
+ * *first_stream runs on first_sms SMs (rounded up to the partition
+ * granularity, count in *first_count), *rest_stream on the remaining
+ * *rest_count SMs.  Created once per process; later calls with the same
+ * first_sms return the same streams. */
+int pearl_green_streams(int first_sms, void** first_stream, void** rest_stream, int* first_count,
+                        int* rest_count);
 
 /* Diagnostic: copy an internal activation buffer of the last forward
  * (0 residual h fp32 [T, d]; 1 x, 2 q, 3 o, 4 act bf16; 5 stream-K tile

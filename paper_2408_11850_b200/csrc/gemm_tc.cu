@@ -336,6 +336,7 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   int dev = 0;
   PEARL_CUDA_TRY(cudaGetDevice(&dev));
   PEARL_CUDA_TRY(cudaDeviceGetAttribute(&ctx.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  if (c.sm_count > 0) ctx.num_sms = std::min(ctx.num_sms, c.sm_count);
   std::call_once(g_attr_once, [] {
     cudaError_t e = set_attr<1>();
     if (e == cudaSuccess) e = set_attr<2>();

@@ -48,6 +48,12 @@ struct LayerW {
 };
 
 
+struct L2Window {
+  const void* base = nullptr;
+  size_t bytes = 0;
+  float hit_ratio = 0.f;
+};
+
 struct Llama {
   pearl_llama_config cfg;
   const bf16* embed;
@@ -58,6 +64,7 @@ struct Llama {
   bf16* kcache;
   bf16* vcache;
   std::vector<LayerW> layers;
+  L2Window l2win;         // optional persisting-L2 window over the streamed weights
   // workspace
   float* h = nullptr;     // [T, d]
   bf16* x = nullptr;      // [T, max(d, ffn, H hd)]
@@ -97,6 +104,12 @@ enum ProfOp { OP_EMBED = 0, OP_NORM, OP_QKV, OP_ATTN, OP_O, OP_GU, OP_DOWN, OP_H
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// L2 access-policy window attached to every launch of the model currently
+// running a forward (pearl_llama_set_l2_window): its streamed weights are
+// kept L2-resident (persisting lines), so a draft's per-token weight reads
+// are served from L2 instead of competing with the target for HBM.
+L2Window g_l2win;  // set for the duration of pearl_llama_forward
+
 template <typename... KArgs, typename... Args>
 int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -104,11 +117,24 @@ int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (g_l2win.bytes > 0) {
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = const_cast<void*>(g_l2win.base);
+    at[na].val.accessPolicyWindow.num_bytes = g_l2win.bytes;
+    at[na].val.accessPolicyWindow.hitRatio = g_l2win.hit_ratio;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = na;
   PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
   count_launch();
   return PEARL_OK;
@@ -191,7 +217,6 @@ __global__ void advance_kernel(int32_t* pos, int n) {
 // per (row, token) in fp32, then a fixed xor-shuffle tree reduces the lanes.
 // ---------------------------------------------------------------------------
 constexpr int kGemvRows = 4;
-constexpr int kGemvTok = 8;
 constexpr int kGemvWarps = 8;
 
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
@@ -223,6 +248,10 @@ struct GemvNorm {
 
 constexpr int kGemvMaxNormTok = 64;
 
+// TOK: tokens accumulated per pass (1 for single-token decode: fewer live
+// registers, more loads in flight; 8 otherwise).  Per-token arithmetic is
+// the same for every TOK (batch invariance).
+template <int TOK>
 __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __restrict__ W, const bf16* __restrict__ X,
                                                                int M, int N, int K, EpiArgs e, GemvNorm nrm) {
   __shared__ float s_rs[kGemvMaxNormTok];
@@ -233,12 +262,23 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
     for (int t = warp; t < M; t += kGemvWarps) {
       const float4* hr = reinterpret_cast<const float4*>(nrm.xh + static_cast<size_t>(t) * K);
       float ss = 0.f;
-      for (int j = lane; j < K / 4; j += 32) {
-        const float4 v = hr[j];
-        ss = fmaf(v.x, v.x, ss);
-        ss = fmaf(v.y, v.y, ss);
-        ss = fmaf(v.z, v.z, ss);
-        ss = fmaf(v.w, v.w, ss);
+      // 8 float4 loads in flight per lane, then summed in j order
+      for (int j0 = lane; j0 < K / 4; j0 += 32 * 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + 32 * u;
+          v[u] = j < K / 4 ? hr[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (j0 + 32 * u < K / 4) {
+            ss = fmaf(v[u].x, v[u].x, ss);
+            ss = fmaf(v[u].y, v[u].y, ss);
+            ss = fmaf(v[u].z, v[u].z, ss);
+            ss = fmaf(v[u].w, v[u].w, ss);
+          }
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -249,14 +289,14 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
   const int n0 = (blockIdx.x * kGemvWarps + warp) * kGemvRows;
   if (n0 >= N) return;
   const int nchunk = (K + 255) / 256;
-  for (int t0 = 0; t0 < M; t0 += kGemvTok) {
-    const int mt = min(kGemvTok, M - t0);
-    float acc[kGemvRows][kGemvTok];
+  for (int t0 = 0; t0 < M; t0 += TOK) {
+    const int mt = min(TOK, M - t0);
+    float acc[kGemvRows][TOK];
 #pragma unroll
     for (int r = 0; r < kGemvRows; ++r)
 #pragma unroll
-      for (int t = 0; t < kGemvTok; ++t) acc[r][t] = 0.f;
-#pragma unroll 2
+      for (int t = 0; t < TOK; ++t) acc[r][t] = 0.f;
+#pragma unroll(TOK == 1 ? 4 : 2)
     for (int c = 0; c < nchunk; ++c) {
       const int k = c * 256 + lane * 8;
       if (k < K) {
@@ -274,7 +314,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
           gk[4] = g1.x; gk[5] = g1.y; gk[6] = g1.z; gk[7] = g1.w;
         }
 #pragma unroll
-        for (int t = 0; t < kGemvTok; ++t) {
+        for (int t = 0; t < TOK; ++t) {
           if (t < mt) {
             float xv[8];
             if (nrm.xh != nullptr) {
@@ -299,7 +339,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
 #pragma unroll
     for (int r = 0; r < kGemvRows; ++r)
 #pragma unroll
-      for (int t = 0; t < kGemvTok; ++t)
+      for (int t = 0; t < TOK; ++t)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[r][t] += __shfl_xor_sync(0xffffffffu, acc[r][t], o);
     if (lane == 0) {
@@ -492,8 +532,9 @@ int attention_tpb(int M, int H) {
 int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
                 GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
   const int rows_per_block = kGemvWarps * kGemvRows;
-  return launch_pdl(gemv_kernel, dim3((N + rows_per_block - 1) / rows_per_block), dim3(kGemvWarps * 32), 0, st, W, X,
-                    M, N, K, e, nrm);
+  const dim3 grid((N + rows_per_block - 1) / rows_per_block);
+  if (M == 1) return launch_pdl(gemv_kernel<1>, grid, dim3(kGemvWarps * 32), 0, st, W, X, M, N, K, e, nrm);
+  return launch_pdl(gemv_kernel<8>, grid, dim3(kGemvWarps * 32), 0, st, W, X, M, N, K, e, nrm);
 }
 
 static int ablate_mask();
@@ -963,6 +1004,10 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
   const bool last_only = (flags & PEARL_FWD_LAST_LOGITS) != 0;
   PEARL_ARG_CHECK(last_only || n_tokens <= T || logits == nullptr,
                   "windows longer than max_tokens need PEARL_FWD_LAST_LOGITS");
+  struct WindowScope {
+    explicit WindowScope(const L2Window& w) { g_l2win = w; }
+    ~WindowScope() { g_l2win = L2Window{}; }
+  } window_scope(m->l2win);
   for (int c0 = 0; c0 < n_tokens; c0 += T) {
     const int mt = std::min(T, n_tokens - c0);
     const bool last_chunk = c0 + mt == n_tokens;
@@ -974,6 +1019,35 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
     int rc = launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, pos, n_tokens);
     if (rc) return rc;
   }
+  return PEARL_OK;
+}
+
+extern "C" int pearl_llama_set_l2_window(void* handle, const void* base, size_t bytes, size_t* granted) {
+  Llama* m = static_cast<Llama*>(handle);
+  PEARL_ARG_CHECK(m != nullptr, "null handle");
+  if (base == nullptr || bytes == 0) {
+    m->l2win = L2Window{};
+    if (granted) *granted = 0;
+    return PEARL_OK;
+  }
+  int dev = 0, max_persist = 0, max_window = 0;
+  PEARL_CUDA_TRY(cudaGetDevice(&dev));
+  PEARL_CUDA_TRY(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  PEARL_CUDA_TRY(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+  if (max_persist <= 0 || max_window <= 0) {
+    m->l2win = L2Window{};
+    if (granted) *granted = 0;
+    return PEARL_OK;
+  }
+  size_t cur = 0;
+  PEARL_CUDA_TRY(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  const size_t want = std::min(bytes, static_cast<size_t>(max_persist));
+  if (want > cur) PEARL_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+  PEARL_CUDA_TRY(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  m->l2win.base = base;
+  m->l2win.bytes = std::min(bytes, static_cast<size_t>(max_window));
+  m->l2win.hit_ratio = std::min(1.0f, static_cast<float>(cur) / static_cast<float>(m->l2win.bytes));
+  if (granted) *granted = cur;
   return PEARL_OK;
 }
 

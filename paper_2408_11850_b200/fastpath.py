@@ -23,6 +23,7 @@ reference's tokens and traces.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import replace
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -109,8 +110,16 @@ class PairRuntime:
         self.graphs: Dict[tuple, torch.cuda.CUDAGraph] = {}
         self.graph_launches: Dict[tuple, int] = {}
         self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        self.draft_stream = torch.cuda.Stream(device=dev, priority=-1)
-        self.target_stream = torch.cuda.Stream(device=dev)
+        green = getattr(target, "green_partition", None)
+        if green is not None:
+            # each model on its own SM partition (llama.build_pair(draft_sms=...))
+            self.draft_stream = torch.cuda.ExternalStream(green[0], device=dev)
+            self.target_stream = torch.cuda.ExternalStream(green[1], device=dev)
+        else:
+            # shared SMs: stream priorities of the two concurrent models (PEARL_PRIO: draft | target | none)
+            prio = os.environ.get("PEARL_PRIO", "draft")
+            self.draft_stream = torch.cuda.Stream(device=dev, priority=-1 if prio == "draft" else 0)
+            self.target_stream = torch.cuda.Stream(device=dev, priority=-1 if prio == "target" else 0)
         self.lib = _lib.load()
         _lib.prepare_vocab(V)
 
@@ -328,9 +337,14 @@ class _GammaPlanner:
         key = "_pearl_calib_" + str(id(draft))
         cal = target.__dict__.get(key)
         if cal is None:
-            t_d = draft.measure_forward_time(1) + 6e-6  # + the pick kernel
+            green = getattr(target, "green_partition", None)
+            sd = torch.cuda.ExternalStream(green[0]) if green else torch.cuda.current_stream()
+            st = torch.cuda.ExternalStream(green[1]) if green else torch.cuda.current_stream()
+            with torch.cuda.stream(sd):  # each model timed where PEARL runs it
+                t_d = draft.measure_forward_time(1) + 6e-6  # + the pick kernel
             ms = [1, 8, 16, 32]
-            t_t = {m: target.measure_forward_time(m) for m in ms}
+            with torch.cuda.stream(st):
+                t_t = {m: target.measure_forward_time(m) for m in ms}
             cal = (t_d, t_t)
             target.__dict__[key] = cal
         self.t_d, self.t_t = cal

@@ -32,6 +32,7 @@ acceptance is always reported next to any speedup.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 import time
 from dataclasses import dataclass, replace
@@ -179,10 +180,30 @@ def init_pair(pair: str, align: AlignSpec = AlignSpec(), device=None):
 class _CConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "ffn",
                                               "vocab", "max_seq", "max_tokens", "gemm_kind")] + [
-        ("norm_eps", ctypes.c_float), ("reserved", ctypes.c_float)]
+        ("norm_eps", ctypes.c_float), ("sm_count", ctypes.c_int32)]
 
 
 GEMM_KINDS = {"cudacore": 0, "tcgen05": 1}
+
+
+def _pack_streamed(w: Dict[str, object]):
+    """Copy every per-token streamed tensor (lm_head, final norm, all layer
+    weights; not the embedding table, which is only gathered) into one
+    contiguous device buffer and point ``w`` at views of it."""
+    items = [(w, "lm_head"), (w, "final_norm")]
+    for L in w["layers"]:
+        items += [(L, k) for k in ("attn_norm", "wqkv", "wo", "mlp_norm", "w_gate_up", "w_down")]
+    offs, total = [], 0
+    for d, k in items:
+        offs.append(total)
+        total += (d[k].numel() * d[k].element_size() + 255) // 256 * 256
+    buf = torch.empty(total, dtype=torch.uint8, device=w["lm_head"].device)
+    for (d, k), off in zip(items, offs):
+        t = d[k]
+        v = buf[off:off + t.numel() * t.element_size()].view(t.dtype).view(t.shape)
+        v.copy_(t)
+        d[k] = v
+    return buf, total
 
 
 class LlamaModel(SequenceModel):
@@ -192,7 +213,7 @@ class LlamaModel(SequenceModel):
 
     def __init__(self, cfg: LlamaConfig, weights: Dict[str, object], gemm: str = "cudacore",
                  max_seq: int = 1024, max_tokens: int = 64, temperature: float = 1.0, bos_id: int = 1,
-                 latency: Optional[LatencyProfile] = None):
+                 latency: Optional[LatencyProfile] = None, l2_resident: bool = False, sm_count: int = 0):
         self.device = _device.require_cuda()
         self.cfg = cfg
         self.vocab_size = cfg.vocab
@@ -202,6 +223,8 @@ class LlamaModel(SequenceModel):
         self.max_tokens = int(max_tokens)
         self.gemm = gemm
         self.w = weights
+        # streamed weights packed contiguously so one L2 access-policy window covers them
+        self._l2_pack = _pack_streamed(weights) if l2_resident else None
         hd = cfg.head_dim
         cos, sin = rope_tables(hd, max_seq, cfg.rope_theta)
         self.rope_cos = torch.from_numpy(cos).to(self.device)
@@ -217,11 +240,18 @@ class LlamaModel(SequenceModel):
             assert t.is_cuda and t.is_contiguous()
         self._ptr_arr = (ctypes.c_void_p * len(ptrs))(*[t.data_ptr() for t in ptrs])
         c = _CConfig(cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.n_kv_heads, hd, cfg.ffn, cfg.vocab, max_seq,
-                     max_tokens, GEMM_KINDS[gemm], cfg.norm_eps, 0.0)
+                     max_tokens, GEMM_KINDS[gemm], cfg.norm_eps, int(sm_count))
         h = ctypes.c_void_p()
         _lib.check(_lib.load().pearl_llama_create(ctypes.byref(c), self._ptr_arr, len(ptrs), ctypes.byref(h)),
                    "pearl_llama_create")
         self.handle = h
+        self.l2_granted = 0
+        if self._l2_pack is not None:
+            buf, nbytes = self._l2_pack
+            granted = ctypes.c_size_t(0)
+            _lib.check(_lib.load().pearl_llama_set_l2_window(h, buf.data_ptr(), nbytes, ctypes.byref(granted)),
+                       "pearl_llama_set_l2_window")
+            self.l2_granted = int(granted.value)
         _lib.prepare_vocab(cfg.vocab)
         # adapter state (next_dist): tokens whose K/V occupy cache positions 0..n-1
         self._pos = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -331,11 +361,42 @@ def inv_temp(t: float) -> float:
     return float(np.float32(1.0 / t))
 
 
-def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: str = "cudacore",
+def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: str = "auto",
                align: AlignSpec = AlignSpec(), max_seq: int = 1024, max_tokens: int = 64,
-               temperature: float = 1.0):
-    """(target LlamaModel, draft LlamaModel) with controlled-alignment random weights."""
+               temperature: float = 1.0, l2_draft: Optional[bool] = None, draft_sms: Optional[int] = None):
+    """(target LlamaModel, draft LlamaModel) with controlled-alignment random weights.
+
+    ``l2_draft``: keep the draft's streamed weights in persisting L2
+    (PEARL_L2_DRAFT, default off).  ``draft_sms``: run PEARL's concurrent
+    draft on its own partition of that many SMs and the target on the rest
+    (green contexts; PEARL_DRAFT_SMS, default 0 = shared SMs).  The target's
+    stream-K grids are then sized to its partition for every engine, so AR,
+    SD and PEARL stay bitwise consistent.  ``gemm_draft="auto"``: the CUDA-core
+    GEMV (K2) for drafts under 1 GB of weights, where a forward is
+    launch-latency bound and K2 is as fast; tcgen05 (K3) for larger drafts,
+    where it streams faster (tools/draft_times.py: 1.3B 1.21 vs 1.50 ms,
+    8B 3.41 vs 4.51 ms per token on B200)."""
+    if l2_draft is None:
+        l2_draft = os.environ.get("PEARL_L2_DRAFT", "0") == "1"
+    if draft_sms is None:
+        draft_sms = int(os.environ.get("PEARL_DRAFT_SMS", "0"))
+    green = None
+    target_sms = 0
+    if draft_sms > 0:
+        _device.require_cuda()
+        ds, ts = ctypes.c_void_p(), ctypes.c_void_p()
+        nd, nt = ctypes.c_int(0), ctypes.c_int(0)
+        _lib.check(_lib.load().pearl_green_streams(int(draft_sms), ctypes.byref(ds), ctypes.byref(ts), ctypes.byref(nd),
+                                                   ctypes.byref(nt)), "pearl_green_streams")
+        green = (ds.value, ts.value, nd.value, nt.value)
+        target_sms = nt.value
     tw, dw, tc, dc = init_pair(pair, align)
-    target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature)
-    draft = LlamaModel(dc, dw, gemm=gemm_draft, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature)
+    target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature,
+                        sm_count=target_sms)
+    if gemm_draft == "auto":
+        gemm_draft = "tcgen05" if dc.weight_bytes() > 1e9 else "cudacore"
+    draft = LlamaModel(dc, dw, gemm=gemm_draft, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature,
+                       l2_resident=l2_draft)
+    if green is not None:
+        target.green_partition = green  # (draft stream, target stream, draft SMs, target SMs)
     return target, draft

@@ -6,8 +6,11 @@ import numpy as np, torch
 from paper_2408_11850_b200 import llama, fastpath, _lib, _device
 pair = sys.argv[1] if len(sys.argv) > 1 else "llama2-7b/68m"
 gammas = [int(g) for g in sys.argv[2].split(",")] if len(sys.argv) > 2 else [4, 8, 12, 16, 24]
-target, draft = llama.build_pair(pair, gemm_target="tcgen05", align=llama.AlignSpec(branch_std=5e-4),
+dg = os.environ.get("DRAFT_GEMM", "cudacore")
+target, draft = llama.build_pair(pair, gemm_target="tcgen05", gemm_draft=dg, align=llama.AlignSpec(branch_std=5e-4),
                                  max_seq=600, max_tokens=64)
+print(f"{pair}: draft gemm {dg}: draft fwd {draft.measure_forward_time(1)*1e3:.3f} ms, target fwd M=1 "
+      f"{target.measure_forward_time(1)*1e3:.3f} ms", flush=True)
 rt = fastpath._runtime(target, draft, 32)
 rng = np.random.default_rng(0)
 seq0 = [target.bos_id] + rng.integers(2, target.cfg.vocab, 127).tolist()
