@@ -57,9 +57,9 @@ namespace pearl {
 constexpr int kMgThreads = 224;  // 7 warps
 constexpr int kMgEpiWarp0 = 2;
 constexpr int kMgXWarp = 6;
-constexpr int kMgStages = 5;
+constexpr int kMgStages = 8;
 constexpr int kMgStageBytes = kWBytes + kXBytes;        // NT = 1
-constexpr int kMgRing = kMgStages * kMgStageBytes;      // 90 KB
+constexpr int kMgRing = kMgStages * kMgStageBytes;      // 144 KB
 constexpr int kMgEBytes = kTileN * 16 * 4;               // [128][16] fp32
 constexpr int kMgAttnWarps = 4;
 constexpr int kMgChunk = 32;

@@ -22,13 +22,15 @@ constexpr int kTcThreads = 192;
 constexpr int kEpiThreads = 128;
 constexpr int kAccs = 4;  // TMEM accumulators (x NT*16 fp32 columns) in flight
 
-// Per token-tile-count (NT) configuration.  NT <= 2 keeps smem <= ~100 KB and
-// registers <= 168/thread so two CTAs fit on an SM: the next kernel's CTAs
-// (programmatic dependent launch) then co-reside and stream their first
-// weight stages while this kernel drains.
+// Per token-tile-count (NT) configuration.  One CTA per SM with a deep ring
+// (8 stages of 16 KB weight tiles in flight per SM) beats two co-resident
+// CTAs with a 90 KB ring (which let the next kernel's CTAs start streaming
+// under programmatic dependent launch): 7B forward M=4 3.43 -> 3.31 ms,
+// M=16 4.0 -> 3.77 ms, M=24 5.15 -> 4.35 ms (B200, graph replay).  A
+// 200 KB / 12-stage ring measured no better.
 template <int NT>
 struct TcCfg {
-  static constexpr int kRing = NT <= 2 ? 90 * 1024 : 144 * 1024;
+  static constexpr int kRing = 144 * 1024;
   static constexpr int kStageBytes = kWBytes + NT * kXBytes;
   static constexpr int kStages = (kRing / kStageBytes) < kMaxStages ? (kRing / kStageBytes) : kMaxStages;
   static constexpr int kEStride = NT * 16;                 // fp32 per staged row
@@ -36,7 +38,7 @@ struct TcCfg {
   static constexpr int kCols = kAccs * NT * 16;
   static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + kEBytes + 512;
-  static constexpr int kMinBlocks = NT <= 2 ? 2 : 1;
+  static constexpr int kMinBlocks = 1;
 };
 
 

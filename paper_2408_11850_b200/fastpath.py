@@ -116,8 +116,10 @@ class PairRuntime:
             self.draft_stream = torch.cuda.ExternalStream(green[0], device=dev)
             self.target_stream = torch.cuda.ExternalStream(green[1], device=dev)
         else:
-            # shared SMs: stream priorities of the two concurrent models (PEARL_PRIO: draft | target | none)
-            prio = os.environ.get("PEARL_PRIO", "draft")
+            # shared SMs: stream priorities of the two concurrent models (PEARL_PRIO: draft | target |
+            # none).  Equal priorities measured best with the 1-CTA/SM deep-ring GEMMs (7B/68M
+            # post-verify step, gamma 16: none 4.37 ms, draft-first 4.63, target-first 4.93).
+            prio = os.environ.get("PEARL_PRIO", "none")
             self.draft_stream = torch.cuda.Stream(device=dev, priority=-1 if prio == "draft" else 0)
             self.target_stream = torch.cuda.Stream(device=dev, priority=-1 if prio == "target" else 0)
         self.lib = _lib.load()
