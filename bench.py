@@ -342,7 +342,8 @@ def run_reference(args):
     torch.set_num_threads(cores)
     tname, dname = PAIRS[args.pair]
     tc, dc = PRESETS[tname], PRESETS[dname]
-    align = AlignSpec(branch_std=args.branch_std, kappa=args.kappa)
+    align = AlignSpec(branch_std=args.branch_std if args.branch_std is not None else PAIR_BRANCH_STD[args.pair],
+                      kappa=args.kappa)
     # weights are generated where it is fast (the GPU when present: same
     # values as the GPU arm) and then moved to host memory; only the CPU
     # decode below is timed.
