@@ -38,6 +38,7 @@ extern "C" {
 #define PEARL_ERR_ALL_ZERO_RESIDUAL 2    /* core.AllZeroResidual     */
 #define PEARL_ERR_ZERO_DRAFT_PROB 3      /* core.ZeroDraftProb       */
 #define PEARL_ERR_VALUE 4                /* ValueError (bad lengths, exhausted uniforms) */
+#define PEARL_ERR_TIMEOUT 5              /* split pair: the peer never delivered (DeviceError) */
 #define PEARL_ERR_CUDA (-1)
 #define PEARL_ERR_ARG (-2)
 
@@ -267,6 +268,60 @@ int pearl_pearl_commit(const pearl_commit_args* args, void* stream);
  * committed+pending [draft_pos ..]. */
 int pearl_step_assemble(pearl_seq_state* state, const int32_t* seq_tokens, const int32_t* pending_tok,
                         int32_t* target_in, int32_t* draft_in, int32_t* draft_in_count, void* stream);
+
+/* ======================================================================== *
+ * K6 -- split pair: draft and target on different GPUs (one process each).
+ * Replaces the _PhaseRunner rendezvous (engines.py:241-262) when the two
+ * closures run on different devices: the draft rank pushes its gamma ids and
+ * q-logit rows into a mailbox in the TARGET GPU's memory, the target rank
+ * verifies (K1) and pushes the verdict into a mailbox in the DRAFT GPU's
+ * memory.  Mailboxes are plain device allocations shared through CUDA IPC
+ * (peer-mapped over NVLink / NVSwitch); push and wait are kernels, so a
+ * split step stays one CUDA graph per rank.
+ *
+ * Mailbox layout: [0, 8) uint64 sequence flag; ids int32 at
+ * PEARL_MAILBOX_IDS_OFFSET (<= PEARL_MAILBOX_MAX_IDS); fp32 rows at
+ * PEARL_MAILBOX_ROWS_OFFSET (16-byte aligned).
+ * ======================================================================== */
+#define PEARL_MAILBOX_IDS_OFFSET 256
+#define PEARL_MAILBOX_MAX_IDS 1024
+#define PEARL_MAILBOX_ROWS_OFFSET (256 + 4 * 1024)
+#define PEARL_IPC_HANDLE_BYTES 64
+
+/* Bytes of a mailbox holding n_rows fp32 rows of V (plus header and ids). */
+size_t pearl_mailbox_bytes(int n_rows, int V);
+/* Setup calls (allocate / synchronise): a zeroed mailbox in the current
+ * device's memory, and its release. */
+int pearl_mailbox_alloc(size_t bytes, void** dptr);
+int pearl_mailbox_free(void* dptr);
+/* CUDA-IPC export of a mailbox (64 opaque bytes into host handle_out) and
+ * import of a peer's handle (maps the peer allocation, enabling NVLink peer
+ * access); the importing process must be a different process. */
+int pearl_ipc_export(void* dptr, void* handle_out);
+int pearl_ipc_import(const void* handle, void** dptr);
+int pearl_ipc_close(void* dptr);
+
+typedef struct {
+  void* peer_box;                /* receiver's mailbox (peer-mapped)          */
+  const int32_t* ids;            /* n_ids int32 -> box ids                    */
+  int32_t n_ids;
+  const float* rows;             /* n_rows x V fp32, contiguous -> box rows   */
+  int32_t n_rows;
+  int32_t V;
+  unsigned long long* send_seq;  /* sender's device counter (starts at 0)     */
+  unsigned int* arrive;          /* sender's zeroed device int (CTA election) */
+} pearl_xfer_send_args;
+
+/* One push: copy ids and rows into the peer mailbox, then release
+ * ++(*send_seq) into its flag (system-scope fence before the flag store). */
+int pearl_xfer_send(const pearl_xfer_send_args* args, void* stream);
+
+/* One receive: spin (acquire, system scope) until the local mailbox's flag
+ * reaches ++(*recv_seq), then copy n_ids ids out of it into dst_ids.  If
+ * timeout_ns > 0 and the flag does not arrive in time, *status (optional)
+ * becomes PEARL_ERR_TIMEOUT and the kernel returns (no GPU hang). */
+int pearl_xfer_wait(const void* box, unsigned long long* recv_seq, int32_t* dst_ids, int n_ids,
+                    int32_t* status, long long timeout_ns, void* stream);
 
 #ifdef __cplusplus
 }

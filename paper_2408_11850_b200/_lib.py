@@ -18,6 +18,7 @@ PEARL_ERR_INVALID_DISTRIBUTION = 1
 PEARL_ERR_ALL_ZERO_RESIDUAL = 2
 PEARL_ERR_ZERO_DRAFT_PROB = 3
 PEARL_ERR_VALUE = 4
+PEARL_ERR_TIMEOUT = 5
 
 ROWS_PROBS64 = 0
 ROWS_LOGITS32 = 1
@@ -69,7 +70,21 @@ SIGNATURES = {
     "pearl_kv_rollback": (_i32, [_vp, _vp, _i32, _vp]),
     "pearl_pearl_commit": (_i32, [_vp, _vp]),
     "pearl_step_assemble": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    # K6 split-pair exchange (csrc/exchange.cu)
+    "pearl_mailbox_bytes": (_sz, [_i32, _i32]),
+    "pearl_mailbox_alloc": (_i32, [_sz, _vp]),
+    "pearl_mailbox_free": (_i32, [_vp]),
+    "pearl_ipc_export": (_i32, [_vp, _vp]),
+    "pearl_ipc_import": (_i32, [_vp, _vp]),
+    "pearl_ipc_close": (_i32, [_vp]),
+    "pearl_xfer_send": (_i32, [_vp, _vp]),
+    "pearl_xfer_wait": (_i32, [_vp, _vp, _vp, _i32, _vp, ctypes.c_longlong, _vp]),
 }
+
+MAILBOX_IDS_OFFSET = 256
+MAILBOX_MAX_IDS = 1024
+MAILBOX_ROWS_OFFSET = 256 + 4 * 1024
+IPC_HANDLE_BYTES = 64
 
 _lock = threading.Lock()
 _lib = None
@@ -110,6 +125,8 @@ def check(code: int, what: str = "") -> None:
         raise ZeroDraftProb(f"{what}: drafted token has zero draft probability")
     if code == PEARL_ERR_VALUE:
         raise ValueError(f"{what}: invalid value")
+    if code == PEARL_ERR_TIMEOUT:
+        raise DeviceError(f"{what}: split-pair peer did not deliver before the exchange timeout")
     msg = load().pearl_last_error()
     raise DeviceError(f"{what}: libpearl_b200 error {code}: {msg.decode() if msg else ''}")
 

@@ -43,7 +43,8 @@ __global__ void commit_kernel(pearl_commit_args a) {
   const bool ok = v.status == PEARL_OK;
   const bool full_accept = ok && v.correction < 0;
   // carry the unverified fresh drafts' q rows over as the next pending block
-  if (!a.sd_mode && full_accept && blockIdx.x < a.gamma - 1) {
+  // (pending_rows == NULL: the draft rank of a split pair, which keeps no q rows)
+  if (!a.sd_mode && full_accept && a.pending_rows && blockIdx.x < a.gamma - 1) {
     const float4* src = reinterpret_cast<const float4*>(a.draft_rows + static_cast<size_t>(blockIdx.x + 1) * a.V);
     float4* dst = reinterpret_cast<float4*>(a.pending_rows + static_cast<size_t>(blockIdx.x) * a.V);
     for (int i = threadIdx.x; i < a.V / 4; i += blockDim.x) dst[i] = src[i];
@@ -114,7 +115,10 @@ __global__ void assemble_kernel(pearl_seq_state* state, const int32_t* seq, cons
                                 int32_t* target_in, int32_t* draft_in, int32_t* draft_in_count) {
   const pearl_seq_state s = *state;
   const int C = s.committed_len, k = s.n_pending;
-  for (int i = threadIdx.x; i <= k; i += blockDim.x) target_in[i] = (i == 0) ? seq[C - 1] : pending[i - 1];
+  // a split pair's ranks assemble only their own model's input (the other pointer is NULL)
+  if (target_in)
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) target_in[i] = (i == 0) ? seq[C - 1] : pending[i - 1];
+  if (!draft_in) return;
   const int cnt = C + k - s.draft_pos;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
     const int idx = s.draft_pos + i;
@@ -138,7 +142,7 @@ extern "C" int pearl_kv_rollback(int32_t* cache_len, const int32_t* new_len, int
 extern "C" int pearl_pearl_commit(const pearl_commit_args* args, void* stream) {
   PEARL_ARG_CHECK(args && args->state && args->seq_tokens && args->chain && args->verdict, "bad commit arguments");
   PEARL_ARG_CHECK(args->gamma >= 1, "gamma >= 1");
-  PEARL_ARG_CHECK(args->sd_mode || args->gamma == 1 || (args->pending_tok && args->pending_rows && args->draft_rows),
+  PEARL_ARG_CHECK(args->sd_mode || args->gamma == 1 || (args->pending_tok && (!args->pending_rows || args->draft_rows)),
                   "pending buffers required");
   const int blocks = args->sd_mode ? 1 : (args->gamma > 1 ? args->gamma - 1 : 1);
   commit_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(*args);
@@ -149,7 +153,7 @@ extern "C" int pearl_pearl_commit(const pearl_commit_args* args, void* stream) {
 
 extern "C" int pearl_step_assemble(pearl_seq_state* state, const int32_t* seq_tokens, const int32_t* pending_tok,
                                    int32_t* target_in, int32_t* draft_in, int32_t* draft_in_count, void* stream) {
-  PEARL_ARG_CHECK(state && seq_tokens && target_in && draft_in, "bad assemble arguments");
+  PEARL_ARG_CHECK(state && seq_tokens && (target_in || draft_in), "bad assemble arguments");
   assemble_kernel<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(state, seq_tokens, pending_tok, target_in, draft_in,
                                                                     draft_in_count);
   PEARL_CUDA_TRY(cudaGetLastError());

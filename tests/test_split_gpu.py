@@ -1,0 +1,118 @@
+"""GPU: the split pair (draft and target on different devices, one process
+each, K6 mailboxes over CUDA IPC) reproduces the co-resident fast path.
+
+This box has one GPU, so both ranks run on cuda:0 as two processes (CUDA IPC
+maps the mailboxes within one device exactly as across NVLink peers; the
+handshake goes over gloo).  On an 8-GPU box the same code runs with each rank
+on its own device.  The bar: tokens and StepTraces (kind, drafted,
+accepted_count, correction, finalized_delta) identical to co-resident
+decode_pearl on the same seeds -- greedy and sampled (T=1), fixed gamma --
+and, with adaptive gamma, both ranks return the same result and greedy
+tokens equal the target's AR decode.
+"""
+
+import os
+import socket
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROMPTS = [[5, 17, 300, 9, 44, 1203, 77, 8], [900, 31, 2, 2, 2, 64]]
+NEW = 40
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _strip(res):
+    return (tuple(res.tokens),
+            tuple((t.kind, tuple(t.drafted), t.accepted_count, t.correction, t.finalized_delta) for t in res.steps))
+
+
+def _cases():
+    import paper_2408_11850_b200 as pk
+    out = []
+    for greedy in (True, False):
+        for i, pr in enumerate(PROMPTS):
+            out.append((pr, pk.EngineConfig(gamma=4, max_new_tokens=NEW, seed=11 + i, greedy=greedy,
+                                            gamma_max=8)))
+    out.append((PROMPTS[0], pk.EngineConfig(gamma=3, max_new_tokens=NEW, seed=5, greedy=True,
+                                            adaptive_gamma=True, gamma_max=8)))
+    return out
+
+
+def _worker(rank, port, q):
+    try:
+        sys.path.insert(0, REPO)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2")
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method="env://")
+        import paper_2408_11850_b200 as pk
+        from paper_2408_11850_b200 import llama, split_pair as split
+        role, peer = split.pair_roles(rank, 2)
+        target, draft = llama.build_pair("tiny", gemm_target="tcgen05", max_seq=256, max_tokens=32)
+        local = target if role == split.ROLE_TARGET else draft
+        remote = split.connect_pair(local, role, peer, gamma_max=8, timeout_s=60.0)
+        outs = []
+        for pr, cfg in _cases():
+            if role == split.ROLE_TARGET:
+                r = pk.decode_pearl(remote, target, pr, cfg)
+            else:
+                r = pk.decode_pearl(draft, remote, pr, cfg)
+            outs.append(_strip(r))
+        remote.link.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, outs, None))
+    except Exception as e:  # report instead of hanging the parent
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+
+
+@pytest.fixture(scope="module")
+def split_results():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        rank, outs, err = q.get(timeout=600)
+        assert err is None, f"rank {rank}:\n{err}"
+        got[rank] = outs
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return got
+
+
+def test_both_ranks_agree(split_results):
+    assert split_results[0] == split_results[1]
+
+
+def test_split_matches_coresident(split_results):
+    import paper_2408_11850_b200 as pk
+    from paper_2408_11850_b200 import llama
+    target, draft = llama.build_pair("tiny", gemm_target="tcgen05", max_seq=256, max_tokens=32)
+    for (pr, cfg), got in zip(_cases(), split_results[0]):
+        if cfg.adaptive_gamma:
+            ar = pk.decode_autoregressive(target, pr, cfg)
+            assert got[0] == tuple(ar.tokens)
+            continue
+        want = _strip(pk.decode_pearl(draft, target, pr, cfg))
+        assert got == want, (cfg, got[0], want[0])
