@@ -117,8 +117,12 @@ def run_gpu(args):
     import torch.distributed as dist
 
     ws, rank, local = _dist()
+    # PEARL_BENCH_BACKEND=gloo + fewer GPUs than ranks: a functional run of the
+    # N>1 path on a 1-GPU box (ranks share cuda:0; the numbers mean nothing)
+    backend = os.environ.get("PEARL_BENCH_BACKEND", "nccl")
     if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group(backend, init_method="env://")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     import paper_2408_11850_b200 as pk
     from paper_2408_11850_b200 import _lib, llama
@@ -182,14 +186,21 @@ def run_gpu(args):
     agg = aggregate(results, ws)
     # roofline of the dominant kernel sequence: one target window forward
     rl = roofline(target, draft, args.gamma, args)
+    target_bytes, draft_bytes = target.cfg.weight_bytes(), draft.cfg.weight_bytes()
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(target, draft, prompts[0], args, greedy, temp)
+    split = None
+    if ws >= 2 and ws % 2 == 0 and not args.no_split:
+        # the co-resident replicas are freed first: a split rank hosts one model
+        del target, draft
+        split = split_leg(args, ws, rank, greedy, temp, agg["ar"])
     if rank != 0:
         if ws > 1:
             dist.barrier()
             dist.destroy_process_group()
         return None
+    wbytes = target_bytes + draft_bytes
     dp, ep, wp, tp = agg["pearl"]
     da, ea, wa, ta = agg["ar"]
     ds_, es, wsd, ts_ = agg["sd"]
@@ -215,7 +226,8 @@ def run_gpu(args):
             "adaptive_gamma": not args.fixed_gamma,
             "sd_gamma": args.sd_gamma, "temperature": 0.0 if greedy else temp,
             "target_gemm": args.gemm_target, "parallelism": f"replicas x{ws}",
-            "l2": "weights 13.6 GB >> 126 MB L2: every forward streams HBM (no flush needed)",
+            "l2": f"weights {wbytes / 1e9:.2f} GB vs 126 MB L2: "
+                  + ("every forward streams HBM (no flush needed)" if wbytes > 126e6 else "L2-resident (tiny pair)"),
         },
         "e2e": {"value": round(tp / ep, 2), "unit": UNIT,
                 "h2d_bytes_per_step": 4 * (args.prompt + 1) + 8 * 2 * 4096,
@@ -236,6 +248,7 @@ def run_gpu(args):
         "gpu_launches": int(results["pearl"]["launches"]),
         "exact_cdf_fallbacks": int(results["pearl"]["fallbacks"]),
         "roofline": rl,
+        "split_pair": split,
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
@@ -246,10 +259,81 @@ def run_gpu(args):
     return line
 
 
-def aggregate(results, ws, device="cuda"):
+def split_leg(args, ws, rank, greedy, temp, ar_agg):
+    """N >= 2: ranks (2i, 2i+1) form split pair i -- the target on the even
+    GPU, the draft on the odd one, meeting through K6 mailboxes (NVLink peer
+    memory).  Each pair decodes its own prompts; tokens are counted once per
+    pair (target ranks), time is the max over all ranks."""
+    import gc
+    import torch
+    import torch.distributed as dist
+    import paper_2408_11850_b200 as pk
+    from paper_2408_11850_b200 import llama, split_pair
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    role, peer = split_pair.pair_roles(rank, ws)
+    tname, dname = llama.PAIRS[args.pair]
+    mc = llama.PRESETS[tname if role == split_pair.ROLE_TARGET else dname]
+    need = mc.weight_bytes() * 1.1 + (2 << 30)
+    ok = torch.tensor([1.0 if torch.cuda.mem_get_info()[0] > need else 0.0],
+                      device="cpu" if dist.get_backend() == "gloo" else "cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() < 1:
+        return {"error": "not enough free device memory after the replica leg"}
+    align = llama.AlignSpec(branch_std=args.branch_std if args.branch_std is not None else PAIR_BRANCH_STD[args.pair],
+                            kappa=args.kappa)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    shared = llama._shared_tables(mc.vocab, align, dev)
+    is_t = role == split_pair.ROLE_TARGET
+    w = llama.init_weights(mc, align, align.seed + (1 if is_t else 2), dev, shared)
+    del shared
+    gemm = args.gemm_target if is_t else ("tcgen05" if mc.weight_bytes() > 1e9 else "cudacore")
+    model = llama.LlamaModel(mc, w, gemm=gemm, max_seq=args.prompt + args.new + 2 * args.gamma_max + 16,
+                             max_tokens=64, temperature=1.0 if greedy else temp)
+    gloo = dist.new_group(backend="gloo")
+    remote = split_pair.connect_pair(model, role, peer, gamma_max=args.gamma_max, group=gloo)
+    prompts = _prompts(args.warmup + args.steps, args.prompt, mc.vocab, seed=2000 + rank // 2)
+
+    def run(i):
+        cfg = pk.EngineConfig(gamma=args.gamma, max_new_tokens=args.new, seed=17 + i, greedy=greedy, temperature=temp,
+                              adaptive_gamma=not args.fixed_gamma, gamma_max=args.gamma_max)
+        return pk.decode_pearl(remote, model, prompts[i], cfg) if is_t else pk.decode_pearl(model, remote, prompts[i],
+                                                                                             cfg)
+
+    for i in range(args.warmup):
+        run(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    ev0.record()
+    res = [run(args.warmup + i) for i in range(args.steps)]
+    ev1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    toks = sum(len(r.tokens) for r in res) if is_t else 0
+    steps = [s for r in res for s in r.steps]
+    one = {"pearl": dict(device_s=sum(r.stats["device_s"] for r in res), event_s=ev0.elapsed_time(ev1) / 1e3,
+                         wall_s=wall, tokens=toks)}
+    d, e, wl, t = aggregate(one, ws)["pearl"]
+    remote.link.close()
+    ar_tps_per_gpu = ar_agg[3] / ar_agg[0] / ws
+    return {"pairs": ws // 2, "placement": "target on even GPU, draft on odd GPU, K6 NVLink mailboxes",
+            "tokens_per_s": round(t / d, 2), "e2e_tokens_per_s": round(t / e, 2),
+            "tokens_per_s_per_pair": round(t / d / (ws // 2), 2),
+            "speedup_vs_single_gpu_ar": round(t / d / (ws // 2) / ar_tps_per_gpu, 3),
+            "mean_accepted_tokens_per_target_fwd": round(pk.mean_tokens_per_target_forward(steps), 3),
+            "alpha_hat": round(pk.empirical_acceptance(steps), 4),
+            "gammas": sorted(set(g for r in res for g in r.stats.get("gammas", [])))}
+
+
+def aggregate(results, ws, device=None):
     """(max device s, max event s, max wall s, sum tokens) per engine over ranks."""
     import torch
     import torch.distributed as dist
+    if device is None:
+        device = "cpu" if ws > 1 and dist.get_backend() == "gloo" else "cuda"
     agg = {}
     for kind, r in results.items():
         vals = torch.tensor([r["device_s"], r["event_s"], r["wall_s"], float(r["tokens"])], device=device,
@@ -402,6 +486,7 @@ def main():
     ap.add_argument("--cpu-new", type=int, default=16)
     ap.add_argument("--cpu-prompt", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-split", action="store_true", help="N>=2: skip the split-pair (draft GPU / target GPU) leg")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
