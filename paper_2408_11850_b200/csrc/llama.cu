@@ -249,12 +249,17 @@ struct GemvNorm {
 constexpr int kGemvMaxNormTok = 64;
 
 // TOK: tokens accumulated per pass (1 for single-token decode: fewer live
-// registers, more loads in flight; 8 otherwise).  Per-token arithmetic is
-// the same for every TOK (batch invariance).
-template <int TOK>
+// registers, more loads in flight; 8 otherwise).  RPW: weight rows per warp --
+// 4 for wide layers, 1 for narrow ones (N < ~9.5k: the draft's o / down /
+// qkv / gate_up), which gives 4x the warps so the per-SM load queue stays
+// full; the 4 rows an epilogue needs (SwiGLU / RoPE pairs) are then gathered
+// from 4 warps through shared memory.  Per-row arithmetic (chunk order, FMA
+// order, xor tree) is identical for every TOK and RPW (batch invariance).
+template <int TOK, int RPW>
 __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __restrict__ W, const bf16* __restrict__ X,
                                                                int M, int N, int K, EpiArgs e, GemvNorm nrm) {
   __shared__ float s_rs[kGemvMaxNormTok];
+  __shared__ float s_out[RPW == 1 ? kGemvWarps * TOK : 1];
   pdl_wait();
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -286,23 +291,24 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
     }
     __syncthreads();
   }
-  const int n0 = (blockIdx.x * kGemvWarps + warp) * kGemvRows;
-  if (n0 >= N) return;
+  const int n0 = (blockIdx.x * kGemvWarps + warp) * RPW;
+  const bool active = n0 < N;
+  if (RPW > 1 && !active) return;
   const int nchunk = (K + 255) / 256;
   for (int t0 = 0; t0 < M; t0 += TOK) {
     const int mt = min(TOK, M - t0);
-    float acc[kGemvRows][TOK];
+    float acc[RPW][TOK];
 #pragma unroll
-    for (int r = 0; r < kGemvRows; ++r)
+    for (int r = 0; r < RPW; ++r)
 #pragma unroll
       for (int t = 0; t < TOK; ++t) acc[r][t] = 0.f;
-#pragma unroll(TOK == 1 ? 4 : 2)
+#pragma unroll(TOK == 1 ? (RPW == 1 ? 8 : 4) : 2)
     for (int c = 0; c < nchunk; ++c) {
       const int k = c * 256 + lane * 8;
-      if (k < K) {
-        float w[kGemvRows][8];
+      if (active && k < K) {
+        float w[RPW][8];
 #pragma unroll
-        for (int r = 0; r < kGemvRows; ++r) {
+        for (int r = 0; r < RPW; ++r) {
           const int n = min(n0 + r, N - 1);
           bf16x8_to_f32(ld_nc_v4(W + static_cast<size_t>(n) * K + k), w[r]);
         }
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
               bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(X + static_cast<size_t>(t0 + t) * K + k)), xv);
             }
 #pragma unroll
-            for (int r = 0; r < kGemvRows; ++r)
+            for (int r = 0; r < RPW; ++r)
 #pragma unroll
               for (int j = 0; j < 8; ++j) acc[r][t] = fmaf(w[r][j], xv[j], acc[r][t]);
           }
@@ -337,16 +343,31 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
       }
     }
 #pragma unroll
-    for (int r = 0; r < kGemvRows; ++r)
+    for (int r = 0; r < RPW; ++r)
 #pragma unroll
       for (int t = 0; t < TOK; ++t)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[r][t] += __shfl_xor_sync(0xffffffffu, acc[r][t], o);
-    if (lane == 0) {
-      for (int t = 0; t < mt; ++t) {
-        float v[4] = {acc[0][t], acc[1][t], acc[2][t], acc[3][t]};
-        epilogue4(e, t0 + t, n0, v, N);
+    if (RPW == 4) {
+      if (lane == 0) {
+        for (int t = 0; t < mt; ++t) {
+          float v[4] = {acc[0][t], acc[1 % RPW][t], acc[2 % RPW][t], acc[3 % RPW][t]};
+          epilogue4(e, t0 + t, n0, v, N);
+        }
       }
+    } else {
+      // gather rows 4g..4g+3 (warps 4g'..4g'+3 of this block) for the epilogue
+      if (lane == 0)
+        for (int t = 0; t < TOK; ++t) s_out[warp * TOK + t] = acc[0][t];
+      __syncthreads();
+      const int grp = threadIdx.x / TOK, t = threadIdx.x % TOK;  // (row quad, token)
+      const int nq = blockIdx.x * kGemvWarps + 4 * grp;
+      if (grp < kGemvWarps / 4 && t < mt && nq < N) {
+        float v[4] = {s_out[(4 * grp) * TOK + t], s_out[(4 * grp + 1) * TOK + t], s_out[(4 * grp + 2) * TOK + t],
+                      s_out[(4 * grp + 3) * TOK + t]};
+        epilogue4(e, t0 + t, nq, v, N);
+      }
+      __syncthreads();
     }
   }
 }
@@ -531,10 +552,17 @@ int attention_tpb(int M, int H) {
 
 int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
                 GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
-  const int rows_per_block = kGemvWarps * kGemvRows;
-  const dim3 grid((N + rows_per_block - 1) / rows_per_block);
-  if (M == 1) return launch_pdl(gemv_kernel<1>, grid, dim3(kGemvWarps * 32), 0, st, W, X, M, N, K, e, nrm);
-  return launch_pdl(gemv_kernel<8>, grid, dim3(kGemvWarps * 32), 0, st, W, X, M, N, K, e, nrm);
+  // narrow layers: one row per warp (4x the warps; same per-row arithmetic)
+  const bool narrow = (N + kGemvWarps * kGemvRows - 1) / (kGemvWarps * kGemvRows) < 296;
+  const dim3 block(kGemvWarps * 32);
+  if (narrow) {
+    const dim3 grid((N + kGemvWarps - 1) / kGemvWarps);
+    if (M == 1) return launch_pdl(gemv_kernel<1, 1>, grid, block, 0, st, W, X, M, N, K, e, nrm);
+    return launch_pdl(gemv_kernel<8, 1>, grid, block, 0, st, W, X, M, N, K, e, nrm);
+  }
+  const dim3 grid((N + kGemvWarps * kGemvRows - 1) / (kGemvWarps * kGemvRows));
+  if (M == 1) return launch_pdl(gemv_kernel<1, 4>, grid, block, 0, st, W, X, M, N, K, e, nrm);
+  return launch_pdl(gemv_kernel<8, 4>, grid, block, 0, st, W, X, M, N, K, e, nrm);
 }
 
 static int ablate_mask();
