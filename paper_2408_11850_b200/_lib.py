@@ -28,7 +28,9 @@ F_BONUS = 2
 F_ADVANCE = 4
 F_PROBE = 8
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpearl_b200.so")
+# PEARL_LIB_PATH: a diagnostic build of the same library (e.g. -DPEARL_TRACE_PICK)
+LIB_PATH = os.environ.get("PEARL_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                            "libpearl_b200.so")
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int

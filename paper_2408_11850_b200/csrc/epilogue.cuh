@@ -30,6 +30,9 @@ struct EpiArgs {
   int n_kv;         // KV * hd
   int hd;
   int ld;           // leading dimension of out
+  int32_t* adv_pos; // optional: one thread adds adv_n to *adv_pos once the kernel's
+  int adv_n;        //   inputs are ready (folds the forward's position advance into
+                    //   its last GEMM: every earlier reader of pos has completed)
 };
 
 // The per-element arithmetic, with explicit rounding (no FMA contraction), so

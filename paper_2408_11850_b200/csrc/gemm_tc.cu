@@ -43,6 +43,7 @@ struct TcArgs {
   EpiArgs e;
   float* partials;
   int* flags;
+  int l2_prefetch;  // W tiles past the ring requested into L2 before the PDL wait
 };
 
 // ---- kernel ------------------------------------------------------------------
@@ -108,7 +109,15 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         mbar_expect_tx(&full[it], bytes);
         tma_load_2d(st, &tmW, &full[it], static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN);
       }
+      // and the next tiles into L2: HBM keeps streaming this GEMM's weights
+      // while the predecessor (attention / RMSNorm / GEMM tail) finishes
+      const int npf = min(total, npre + a.l2_prefetch);
+      for (int it = npre; it < npf; ++it) {
+        const long long x = r0 + it;
+        tma_prefetch_l2_2d(&tmW, static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN);
+      }
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (blockIdx.x == 0 && a.e.adv_pos != nullptr) *a.e.adv_pos += a.e.adv_n;
       for (int it = 0; it < npre; ++it) {
         const long long x = r0 + it;
         unsigned char* st = smem + it * stage_bytes;
@@ -241,6 +250,10 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
 }
 
 // ---- host side ---------------------------------------------------------------
+// W tiles per CTA requested into L2 ahead of the ring before the PDL wait
+// (PEARL_L2PF overrides).
+constexpr int kDefaultL2Prefetch = 0;
+
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -346,6 +359,10 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   });
   PEARL_CUDA_TRY(g_attr_err);
   ctx.max_tokens = c.max_tokens;
+  {
+    const char* v = std::getenv("PEARL_L2PF");
+    ctx.l2_prefetch_iters = v ? std::max(0, std::atoi(v)) : kDefaultL2Prefetch;
+  }
   const int hd = c.head_dim;
   const int shapes[5][2] = {{(c.n_heads + 2 * c.n_kv_heads) * hd, c.d_model},
                             {c.d_model, c.n_heads * hd},
@@ -410,6 +427,7 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.e = e;
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;
+  a.l2_prefetch = ctx.l2_prefetch_iters;
   if (static_cast<size_t>(tiles) * a.seg_max * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
       tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");

@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
   __shared__ float s_out[RPW == 1 ? kGemvWarps * TOK : 1];
   pdl_wait();
   pdl_trigger();
+  if (e.adv_pos != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *e.adv_pos += e.adv_n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (nrm.xh != nullptr) {
     for (int t = warp; t < M; t += kGemvWarps) {
@@ -617,7 +618,8 @@ static int stop_after() {
 }
 
 int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_add, bool logits_all,
-                  bool want_logits, float* logits, cudaStream_t st, bool use_mega) {
+                  bool want_logits, float* logits, cudaStream_t st, bool use_mega, int adv_n = 0,
+                  bool* advanced = nullptr) {
   const int abl = ablate_mask();
   const int stop = stop_after();
   int n_ops = 0;
@@ -733,6 +735,11 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   s.kind = EPI_STORE_F32;
   s.out_f32 = logits;
   s.ld = c.vocab;
+  if (adv_n > 0 && stop < 0 && !abl) {
+    s.adv_pos = pos;  // the lm_head GEMM advances pos (no separate advance kernel)
+    s.adv_n = adv_n;
+    if (advanced) *advanced = true;
+  }
   rc = launch_gemm(m, m.lm_head, fuse_norm ? m.x : m.x + static_cast<size_t>(first) * d, rows, c.vocab, d, s, st,
                    fuse_norm ? GemvNorm{m.h + static_cast<size_t>(first) * d, m.final_norm, c.norm_eps}
                              : GemvNorm{nullptr, nullptr, 0.f});
@@ -1036,14 +1043,16 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
     explicit WindowScope(const L2Window& w) { g_l2win = w; }
     ~WindowScope() { g_l2win = L2Window{}; }
   } window_scope(m->l2win);
+  bool advanced = false;
   for (int c0 = 0; c0 < n_tokens; c0 += T) {
     const int mt = std::min(T, n_tokens - c0);
     const bool last_chunk = c0 + mt == n_tokens;
     int rc = forward_chunk(*m, tokens + c0, mt, pos, c0, !last_only, last_chunk && logits != nullptr, logits, st,
-                           (flags & PEARL_FWD_PERSISTENT) != 0 || mega_default());
+                           (flags & PEARL_FWD_PERSISTENT) != 0 || mega_default(),
+                           last_chunk && (flags & PEARL_FWD_ADVANCE) ? n_tokens : 0, &advanced);
     if (rc) return rc;
   }
-  if (flags & PEARL_FWD_ADVANCE) {
+  if ((flags & PEARL_FWD_ADVANCE) && !advanced) {
     int rc = launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, pos, n_tokens);
     if (rc) return rc;
   }

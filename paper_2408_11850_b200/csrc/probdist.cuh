@@ -34,6 +34,16 @@ namespace cg = cooperative_groups;
 
 namespace pearl {
 
+// Phase timestamps of one CTA (diagnostics: built only with -DPEARL_TRACE_PICK,
+// read with pearl_debug_trace).
+#ifdef PEARL_TRACE_PICK
+__device__ long long g_trace[32];
+#define PEARL_TR(k) \
+  do { if (blockIdx.x == 0 && threadIdx.x == 0) g_trace[k] = clock64(); } while (0)
+#else
+#define PEARL_TR(k) do { } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // plan layout (int32), one block of kPlanStride ints per CTA of the cluster
 //   [0] n_leaves [1] n_nodes [2] n_levels [3] lo [4] hi
@@ -107,6 +117,8 @@ __device__ __forceinline__ int warp_or_i(int v) {
 struct Scratch {
   double xchg[2][4];       // cluster exchange, double-buffered (see ClusterCtx)
   int xchg_i[2][4];
+  double gath_d[kMaxCluster * 4];  // gathered values, row r = CTA r
+  int gath_i[kMaxCluster * 4];
   double warp_d[32];
   int warp_i[32];
   int warp_j[32];
@@ -132,57 +144,60 @@ __device__ __forceinline__ void cluster_sync_all() {
   cg::this_cluster().sync();
 }
 
-// Gather up to 4 doubles from every CTA of the cluster.
-__device__ __forceinline__ void cluster_gather_d(ClusterCtx& cc, Scratch& s, const double* v, int nv,
-                                                 double (*out)[4]) {
+// Gather up to 4 values from every CTA of the cluster.  After the cluster
+// barrier, threads (r, k) < (size, 4) each read ONE remote value into the
+// local gather table (row r = CTA r, 4 slots per row), then a block barrier
+// publishes it: one DSMEM round trip per collective instead of every thread
+// walking every rank.  The returned table stays valid until the next gather
+// of the same type (a CTA can only pass the next cluster barrier once all
+// its threads are done with it).
+__device__ __forceinline__ const double* cluster_gather_d(ClusterCtx& cc, Scratch& s, const double* v, int nv) {
   if (threadIdx.x == 0)
     for (int k = 0; k < nv; ++k) s.xchg[cc.parity][k] = v[k];
   if (cc.size == 1) {
     __syncthreads();
-    for (int k = 0; k < nv; ++k) out[0][k] = s.xchg[cc.parity][k];
-    __syncthreads();
+    if (threadIdx.x < nv) s.gath_d[threadIdx.x] = s.xchg[cc.parity][threadIdx.x];
   } else {
     cluster_sync_all();
-    cg::cluster_group cl = cg::this_cluster();
-    for (int r = 0; r < cc.size; ++r) {
-      double* peer = cl.map_shared_rank(&s.xchg[cc.parity][0], r);
-      for (int k = 0; k < nv; ++k) out[r][k] = peer[k];
-    }
+    if (threadIdx.x < cc.size * 4 && (threadIdx.x & 3) < nv)
+      s.gath_d[threadIdx.x] = cg::this_cluster().map_shared_rank(&s.xchg[cc.parity][0], threadIdx.x >> 2)[threadIdx.x & 3];
   }
+  __syncthreads();
   cc.parity ^= 1;
+  return s.gath_d;
 }
 
-__device__ __forceinline__ void cluster_gather_i(ClusterCtx& cc, Scratch& s, const int* v, int nv,
-                                                 int (*out)[4]) {
+__device__ __forceinline__ const int* cluster_gather_i(ClusterCtx& cc, Scratch& s, const int* v, int nv) {
   if (threadIdx.x == 0)
     for (int k = 0; k < nv; ++k) s.xchg_i[cc.parity][k] = v[k];
   if (cc.size == 1) {
     __syncthreads();
-    for (int k = 0; k < nv; ++k) out[0][k] = s.xchg_i[cc.parity][k];
-    __syncthreads();
+    if (threadIdx.x < nv) s.gath_i[threadIdx.x] = s.xchg_i[cc.parity][threadIdx.x];
   } else {
     cluster_sync_all();
-    cg::cluster_group cl = cg::this_cluster();
-    for (int r = 0; r < cc.size; ++r) {
-      int* peer = cl.map_shared_rank(&s.xchg_i[cc.parity][0], r);
-      for (int k = 0; k < nv; ++k) out[r][k] = peer[k];
-    }
+    if (threadIdx.x < cc.size * 4 && (threadIdx.x & 3) < nv)
+      s.gath_i[threadIdx.x] = cg::this_cluster().map_shared_rank(&s.xchg_i[cc.parity][0], threadIdx.x >> 2)[threadIdx.x & 3];
   }
+  __syncthreads();
   cc.parity ^= 1;
+  return s.gath_i;
 }
 
-// balanced top-level combine of C subtree sums (C power of two)
-__device__ __forceinline__ double tree_combine(const double* v, int lo, int hi) {
-  // iterative bottom-up over a power-of-two count, same association as the
-  // recursive halving of numpy's top levels
-  double buf[kMaxCluster];
-  int n = hi - lo;
-  for (int i = 0; i < n; ++i) buf[i] = v[lo + i];
-  while (n > 1) {
-    for (int i = 0; i < n / 2; ++i) buf[i] = __dadd_rn(buf[2 * i], buf[2 * i + 1]);
-    n >>= 1;
+// balanced top-level combine of n (power of two <= 16) subtree sums g[i*stride],
+// bottom-up, the association of numpy's recursive halving at the top levels
+// (fully unrolled: register-resident)
+__device__ __forceinline__ double tree_combine(const double* g, int stride, int n) {
+  double b[kMaxCluster];
+#pragma unroll
+  for (int i = 0; i < kMaxCluster; ++i) b[i] = i < n ? g[i * stride] : 0.0;
+#pragma unroll
+  for (int w = kMaxCluster; w > 1; w >>= 1) {
+    if (n >= w) {
+#pragma unroll
+      for (int i = 0; i < w / 2; ++i) b[i] = __dadd_rn(b[2 * i], b[2 * i + 1]);
+    }
   }
-  return buf[0];
+  return b[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -253,13 +268,8 @@ __device__ void cluster_pairwise(ClusterCtx& cc, Scratch& s, const int* plan, F 
     for (int c = 0; c < kNv; ++c) result[c] = sums[c];
     return;
   }
-  double all[kMaxCluster][4];
-  cluster_gather_d(cc, s, sums, kNv, all);
-  for (int c = 0; c < kNv; ++c) {
-    double v[kMaxCluster];
-    for (int r = 0; r < cc.size; ++r) v[r] = all[r][c];
-    result[c] = tree_combine(v, 0, cc.size);
-  }
+  const double* all = cluster_gather_d(cc, s, sums, kNv);
+  for (int c = 0; c < kNv; ++c) result[c] = tree_combine(all + c, 4, cc.size);
 }
 
 // ---------------------------------------------------------------------------
@@ -278,10 +288,9 @@ __device__ float cluster_max_f(ClusterCtx& cc, Scratch& s, float v) {
   __syncthreads();
   double m = s.res_d[0];
   __syncthreads();
-  double all[kMaxCluster][4];
-  cluster_gather_d(cc, s, &m, 1, all);
+  const double* all = cluster_gather_d(cc, s, &m, 1);
   float out = -INFINITY;
-  for (int r = 0; r < cc.size; ++r) out = fmaxf(out, static_cast<float>(all[r][0]));
+  for (int r = 0; r < cc.size; ++r) out = fmaxf(out, static_cast<float>(all[4 * r]));
   return out;
 }
 
@@ -301,15 +310,13 @@ __device__ int cluster_argmax(ClusterCtx& cc, Scratch& s, double v, int i) {
   double bv = s.res_d[0];
   int bi = s.res_i[0];
   __syncthreads();
-  double allv[kMaxCluster][4];
-  int alli[kMaxCluster][4];
-  cluster_gather_d(cc, s, &bv, 1, allv);
-  cluster_gather_i(cc, s, &bi, 1, alli);
+  const double* allv = cluster_gather_d(cc, s, &bv, 1);
+  const int* alli = cluster_gather_i(cc, s, &bi, 1);
   double best = -1.0;
   int besti = 0x7fffffff;
   for (int r = 0; r < cc.size; ++r) {
-    double x = allv[r][0];
-    int xi = alli[r][0];
+    double x = allv[4 * r];
+    int xi = alli[4 * r];
     if (x > best || (x == best && xi < besti)) { best = x; besti = xi; }
   }
   return besti;
@@ -325,12 +332,18 @@ __device__ int cluster_search(ClusterCtx& cc, Scratch& s, const int* plan, int V
   const int lo = plan[3], hi = plan[4];
   const int len = hi - lo;
   const int nt = blockDim.x;
-  const int per = (len + nt - 1) / nt;
+  // odd chunk length: thread chunks start 8*per bytes apart, so an odd per
+  // spreads a warp's fp64 reads over all banks (an even 16 put all 32 lanes
+  // on one bank pair).  The answer does not depend on the chunking: the scan
+  // is exact up to the rigorous bound delta, and ambiguous draws replay the
+  // sequential scan.
+  const int per = ((len + nt - 1) / nt) | 1;
   const int st = lo + threadIdx.x * per;
   const int en = min(st + per, hi);
   // rigorous bound on |parallel prefix - sequential prefix| for values
   // summing to ~1: (#adds on either chain) * 2^-53, doubled for margin
   const double delta = static_cast<double>(V + 2048) * 2.220446049250313e-16;
+  PEARL_TR(10);
   // 1) chunk totals
   double t = 0.0;
   for (int i = st; i < en; ++i) t = __dadd_rn(t, a(i));
@@ -358,10 +371,11 @@ __device__ int cluster_search(ClusterCtx& cc, Scratch& s, const int* plan, int V
   const double thread_off = __dadd_rn(s.warp_d[w], __dsub_rn(incl, t));
   const double cta_total = s.res_d[1];
   __syncthreads();
-  double allT[kMaxCluster][4];
-  cluster_gather_d(cc, s, &cta_total, 1, allT);
+  PEARL_TR(11);
+  const double* allT = cluster_gather_d(cc, s, &cta_total, 1);
+  PEARL_TR(12);
   double cta_off = 0.0;
-  for (int r = 0; r < cc.rank; ++r) cta_off = __dadd_rn(cta_off, allT[r][0]);
+  for (int r = 0; r < cc.rank; ++r) cta_off = __dadd_rn(cta_off, allT[4 * r]);
   // 3) walk the chunk
   const double ulo = u - delta, uhi = u + delta;
   int cand = 0x7fffffff;
@@ -373,7 +387,12 @@ __device__ int cluster_search(ClusterCtx& cc, Scratch& s, const int* plan, int V
     if (c > uhi) { cand = i; break; }
     if (c >= ulo) amb = 1;
   }
-  // 4) reduce: j = min cand; ambiguity only counts before j
+  PEARL_TR(13);
+  // 4) reduce: j = min cand; ambiguity only counts before j.  Per CTA:
+  // (first local candidate jl, ambiguity in the chunks up to jl); chunks are
+  // in thread order, so the global answer is j = min over CTAs of jl and the
+  // draw is ambiguous iff some CTA starting at or before j flagged it --
+  // one cluster exchange of both values.
   int wc = warp_min_i(cand);
   if (lane == 0) s.warp_i[w] = wc;
   __syncthreads();
@@ -383,13 +402,8 @@ __device__ int cluster_search(ClusterCtx& cc, Scratch& s, const int* plan, int V
     if (threadIdx.x == 0) s.res_i[1] = x;
   }
   __syncthreads();
-  int jloc = s.res_i[1];
-  __syncthreads();
-  int jj[kMaxCluster][4];
-  cluster_gather_i(cc, s, &jloc, 1, jj);
-  int j = 0x7fffffff;
-  for (int r = 0; r < cc.size; ++r) j = min(j, jj[r][0]);
-  int mine = (amb && st <= j) ? 1 : 0;
+  const int jl = s.res_i[1];
+  int mine = (amb && st <= jl) ? 1 : 0;
   int wa = warp_or_i(mine);
   if (lane == 0) s.warp_j[w] = wa;
   __syncthreads();
@@ -399,12 +413,20 @@ __device__ int cluster_search(ClusterCtx& cc, Scratch& s, const int* plan, int V
     if (threadIdx.x == 0) s.res_i[2] = x;
   }
   __syncthreads();
-  int aloc = (lo <= j) ? s.res_i[2] : 0;
+  int both[2] = {jl, s.res_i[2]};
   __syncthreads();
-  int aa[kMaxCluster][4];
-  cluster_gather_i(cc, s, &aloc, 1, aa);
+  PEARL_TR(14);
+  const int* jj = cluster_gather_i(cc, s, both, 2);
+  PEARL_TR(15);
+  int j = 0x7fffffff;
+  for (int r = 0; r < cc.size; ++r) j = min(j, jj[4 * r]);
   int ambiguous = 0;
-  for (int r = 0; r < cc.size; ++r) ambiguous |= aa[r][0];
+  bool starts_before = true;  // CTA r's slice starts at or before j iff no earlier CTA found a candidate
+  for (int r = 0; r < cc.size; ++r) {
+    // (slices are ordered; r's flag already stops at its own first candidate)
+    if (starts_before) ambiguous |= jj[4 * r + 1];
+    starts_before &= (jj[4 * r] == 0x7fffffff);
+  }
   if (!ambiguous) {
     if (used_fallback) *used_fallback = 0;
     return j;
@@ -425,10 +447,9 @@ __device__ int cluster_search(ClusterCtx& cc, Scratch& s, const int* plan, int V
       v2[0] = cc_;
       v2[1] = static_cast<double>(an);
     }
-    double got[kMaxCluster][4];
-    cluster_gather_d(cc, s, v2, 2, got);
-    carry = got[r][0];
-    if (ans < 0) ans = static_cast<int>(got[r][1]);
+    const double* got = cluster_gather_d(cc, s, v2, 2);
+    carry = got[4 * r];
+    if (ans < 0) ans = static_cast<int>(got[4 * r + 1]);
     __syncthreads();
   }
   return ans;

@@ -25,6 +25,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "common.h"
 #include "probdist.cuh"
@@ -57,8 +58,12 @@ struct RowJob {
 
 extern __shared__ __align__(16) unsigned char g_smem[];
 
+// Loads the (static) plan, then waits for the producing kernel (PDL) and lets
+// dependents launch: every kernel here calls it before touching any input.
 __device__ __forceinline__ void load_plan(int* splan, const int* gplan, int rank) {
   for (int i = threadIdx.x; i < kPlanStride; i += blockDim.x) splan[i] = gplan[rank * kPlanStride + i];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __syncthreads();
 }
 
@@ -109,57 +114,103 @@ __device__ int prepare_rows(ClusterCtx& cc, Scratch& s, const int* plan, const R
     __syncthreads();
     return PEARL_OK;
   }
-  // logits: max + validity
+  // logits: max + validity.  One pass over global memory: a thread's
+  // elements (stride kThreads) are all requested before any is used, kept in
+  // registers, and the exp pass below reuses them (NR == 1; slices of up to
+  // 16 * kThreads elements -- V <= 32768 per CTA slice of 8 -- or 36 * kThreads).
+  constexpr int kMaxPer = 36;
+  float xr[NR == 1 ? kMaxPer : 1];
+  const int len = hi - lo;
+  const int per_mode = NR != 1 ? 0 : (len <= 16 * kThreads ? 16 : (len <= kMaxPer * kThreads ? kMaxPer : 0));
   double mv[4];
   int bad_any = 0;
+  auto load_regs = [&](const float* g, float& m, int& bad, auto per_c) {
+    constexpr int PER = decltype(per_c)::value;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = lo + threadIdx.x + u * kThreads;
+      xr[u] = i < hi ? g[i] : -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      if (isnan(xr[u]) || xr[u] == INFINITY) bad = 1;
+      m = fmaxf(m, xr[u]);
+    }
+  };
   for (int r = 0; r < NR; ++r) {
     const float* g = static_cast<const float*>(rows[r]);
     float m = -INFINITY;
     int bad = 0;
-    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      float x = g[i];
-      if (isnan(x) || x == INFINITY) bad = 1;
-      m = fmaxf(m, x);
+    if (per_mode == 16) {
+      load_regs(g, m, bad, std::integral_constant<int, 16>{});
+    } else if (per_mode == kMaxPer) {
+      load_regs(g, m, bad, std::integral_constant<int, (NR == 1 ? kMaxPer : 1)>{});
+    } else {
+      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        float x = g[i];
+        if (isnan(x) || x == INFINITY) bad = 1;
+        m = fmaxf(m, x);
+      }
     }
     block_max_or(s, m, bad);
     mv[r] = m;
     bad_any |= bad;
   }
   mv[NR] = bad_any;
-  double all[kMaxCluster][4];
-  cluster_gather_d(cc, s, mv, NR + 1, all);
+  PEARL_TR(2);
+  const double* all = cluster_gather_d(cc, s, mv, NR + 1);
+  PEARL_TR(3);
   int invalid = 0;
   for (int r = 0; r < NR; ++r) {
     float m = -INFINITY;
     for (int k = 0; k < cc.size; ++k) {
-      m = fmaxf(m, static_cast<float>(all[k][r]));
-      invalid |= (all[k][NR] != 0.0);
+      m = fmaxf(m, static_cast<float>(all[4 * k + r]));
+      invalid |= (all[4 * k + NR] != 0.0);
     }
     norm[r].m = m;
     if (m == -INFINITY) invalid = 1;
   }
   if (invalid) return PEARL_ERR_INVALID_DISTRIBUTION;
+  auto exp_regs = [&](double* sl, float m, auto per_c) {
+    constexpr int PER = decltype(per_c)::value;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = lo + threadIdx.x + u * kThreads;
+      if (i < hi) sl[i - lo] = static_cast<double>(dev_expf(__fmul_rn(__fsub_rn(xr[u], m), job.inv_temp)));
+    }
+  };
   for (int r = 0; r < NR; ++r) {
     const float* g = static_cast<const float*>(rows[r]);
     double* sl = slices[r];
     const float m = norm[r].m;
-    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
-      sl[i - lo] = static_cast<double>(dev_expf(__fmul_rn(__fsub_rn(g[i], m), job.inv_temp)));
+    if (per_mode == 16) {
+      exp_regs(sl, m, std::integral_constant<int, 16>{});
+    } else if (per_mode == kMaxPer) {
+      exp_regs(sl, m, std::integral_constant<int, (NR == 1 ? kMaxPer : 1)>{});
+    } else {
+      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
+        sl[i - lo] = static_cast<double>(dev_expf(__fmul_rn(__fsub_rn(g[i], m), job.inv_temp)));
+    }
   }
   __syncthreads();
   if (!normalize) {
     for (int r = 0; r < NR; ++r) { norm[r].S = 1.0; norm[r].Pn = 1.0; }
     return PEARL_OK;
   }
+  PEARL_TR(4);
   double S[NR];
   cluster_pairwise<NR>(cc, s, plan, [&](int c, int i) { return slices[c][i - lo]; }, S);
-  for (int r = 0; r < NR; ++r) {
-    double* sl = slices[r];
-    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) sl[i - lo] = __ddiv_rn(sl[i - lo], S[r]);
-  }
-  __syncthreads();
+  PEARL_TR(5);
+  PEARL_TR(6);
+  // arr = e / S is formed inside the second pairwise sum's leaf pass (each
+  // element is evaluated exactly once there and written back)
   double Pn[NR];
-  cluster_pairwise<NR>(cc, s, plan, [&](int c, int i) { return slices[c][i - lo]; }, Pn);
+  cluster_pairwise<NR>(cc, s, plan, [&](int c, int i) {
+    const double a = __ddiv_rn(slices[c][i - lo], S[c]);
+    slices[c][i - lo] = a;
+    return a;
+  }, Pn);
+  PEARL_TR(7);
   for (int r = 0; r < NR; ++r) {
     double* sl = slices[r];
     for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) sl[i - lo] = __ddiv_rn(sl[i - lo], Pn[r]);
@@ -420,7 +471,9 @@ __global__ void __launch_bounds__(kThreads) sample_rows_kernel(SampleArgs A) {
   int* plan = reinterpret_cast<int*>(g_smem);
   Scratch& s = *reinterpret_cast<Scratch*>(g_smem + kPlanStride * sizeof(int));
   double* P = reinterpret_cast<double*>(g_smem + kPlanStride * sizeof(int) + sizeof(Scratch));
+  PEARL_TR(0);
   load_plan(plan, A.job.plan, cc.rank);
+  PEARL_TR(1);
   const int lo = plan[3];
   const bool greedy = (A.flags & PEARL_F_GREEDY) != 0;
   const int cur = A.cursor ? *A.cursor : 0;
@@ -439,7 +492,9 @@ __global__ void __launch_bounds__(kThreads) sample_rows_kernel(SampleArgs A) {
                            A.uniforms[cur + row], nullptr);
     }
   }
+  PEARL_TR(20);
   if (cc.size > 1) cluster_sync_all();
+  PEARL_TR(21);
   if (cc.rank != 0 || threadIdx.x != 0) return;
   A.out[row] = tok;
   if (row == 0 && A.append_dst) *A.append_dst = tok;
@@ -545,13 +600,17 @@ int launch_clustered(K kernel, int n_clusters, int C, size_t smem, void* stream,
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch: the kernels load their vocabulary plan
+  // (static) before griddepcontrol.wait, overlapping the producer's tail
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, args));
   count_launch();
   return PEARL_OK;
@@ -577,6 +636,12 @@ int configure_all() {
 }  // namespace pearl
 
 using namespace pearl;
+
+#ifdef PEARL_TRACE_PICK
+extern "C" int pearl_debug_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * 32) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" size_t pearl_verify_work_bytes(int n) {
   return sizeof(WorkHdr) + static_cast<size_t>(std::max(n, 1) + 1) * sizeof(Rec);
