@@ -234,16 +234,18 @@ class PairRuntime:
             self.graphs[key] = g
         return g
 
-    def replay(self, key: tuple, body, stats: dict) -> None:
-        """Replay the step graph for ``key``, timing it on the device."""
+    def replay(self, key: tuple, body, stats: dict) -> float:
+        """Replay the step graph for ``key``, timing it on the device (returns seconds)."""
         g = self.graph(key, body)
         self.ev[0].record()
         g.replay()
         self.ev[1].record()
         self.ev[1].synchronize()
-        stats["device_s"] += self.ev[0].elapsed_time(self.ev[1]) / 1e3
+        t = self.ev[0].elapsed_time(self.ev[1]) / 1e3
+        stats["device_s"] += t
         stats["launches"] += self.graph_launches[key]
         stats["replays"] += 1
+        return t
 
     # -- decode-level helpers ---------------------------------------------------
     def reset(self, seq0: List[int], stats: Optional[dict] = None) -> None:
@@ -327,11 +329,19 @@ def pearl_tokens_per_step(alpha: float, gamma: int) -> float:
 
 class _GammaPlanner:
     """Adaptive draft length (paper §3.4): gamma maximising expected PEARL
-    tokens per unit step time, E(gamma, alpha_hat) / max(t_target(gamma),
-    gamma * t_draft), with t measured once per model pair (CUDA events) and
-    alpha_hat a running Laplace estimate of this decode's acceptance.  The
-    choice depends only on the decode's own history and the cached
-    calibration, so a decode is reproducible within a process."""
+    tokens per unit of device time,
+
+        rate(g) = E(g, alpha_hat) / (pi_pre(g) T_pre(g) + pi_post(g) T_post(g)),
+
+    with E the stationary tokens per step (pearl_tokens_per_step), pi the
+    stationary PRE / POST step shares (pi_post / pi_pre = a / (1 - a^g)) and
+    alpha_hat a running Laplace estimate of this decode's acceptance.  Step
+    times T are the MEASURED device times of that (mode, g) step graph when
+    it has run before (EMA, kept per model pair across decodes), else the
+    contention-free model max(t_target(M), g * t_draft) from one calibration
+    of each model.  On a shared GPU the draft's kernels compete with the
+    target's for SMs and HBM, which the model does not see; the measurements
+    do (7B/68M: the model prices gamma 32 at 4.6 ms, it runs in 7.4 ms)."""
 
     GRID = (1, 2, 3, 4, 6, 8, 12, 16, 20, 24, 32, 48, 64)
 
@@ -350,6 +360,7 @@ class _GammaPlanner:
             cal = (t_d, t_t)
             target.__dict__[key] = cal
         self.t_d, self.t_t = cal
+        self.meas = target.__dict__.setdefault("_pearl_steptimes_" + str(id(draft)), {})
         self.gmax = gamma_max
         self.acc, self.exam = 3.0, 4.0  # prior alpha 0.75
         self.gamma = gamma0
@@ -368,6 +379,25 @@ class _GammaPlanner:
     def observe(self, accepted: int, rejected: int) -> None:
         self.acc += accepted
         self.exam += accepted + rejected
+
+    def observe_time(self, pre: bool, g: int, seconds: float) -> None:
+        """Measured device time of one step graph (co-resident path only: the
+        split pair's two ranks must plan identically, so they use the model)."""
+        k = (bool(pre), int(g))
+        old = self.meas.get(k)
+        self.meas[k] = seconds if old is None else 0.75 * old + 0.25 * seconds
+
+    def step_time(self, pre: bool, g: int) -> float:
+        m = self.meas.get((bool(pre), int(g)))
+        if m is not None:
+            return m
+        return max(self._t_target(1 if pre else g), g * self.t_d)
+
+    def rate(self, alpha: float, g: int) -> float:
+        a = min(max(alpha, 1e-6), 1.0 - 1e-9)
+        post_per_pre = a / (1.0 - a ** g)
+        t = (self.step_time(True, g) + post_per_pre * self.step_time(False, g)) / (1.0 + post_per_pre)
+        return pearl_tokens_per_step(alpha, g) / t
 
     def candidates(self) -> List[int]:
         return [g for g in self.GRID if g <= self.gmax]
@@ -388,7 +418,7 @@ class _GammaPlanner:
         best, best_rate = 1, -1.0
         cands = self.candidates() if not self.started else self.neighbors(self.gamma)
         for g in cands:
-            rate = pearl_tokens_per_step(alpha, g) / max(self._t_target(g), g * self.t_d)
+            rate = self.rate(alpha, g)
             if rate > best_rate:
                 best, best_rate = g, rate
         self.gamma = best
@@ -435,7 +465,9 @@ def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], c
         m0 = len(committed) + k - dpos
         stats["gammas"].append(gamma)
         key = ("pearl", k, gamma, m0, bool(cfg.greedy), invt, bool(concurrent))
-        rt.replay(key, lambda: rt._pearl_body(k, gamma, m0, invt, cfg.greedy, concurrent), stats)
+        t_step = rt.replay(key, lambda: rt._pearl_body(k, gamma, m0, invt, cfg.greedy, concurrent), stats)
+        if planner is not None and m0 == 1:
+            planner.observe_time(k == 0, gamma, t_step)
         s = rt.summary_host.numpy()
         status = int(s[SUM_STATUS])
         _lib.check(status, "decode_pearl step")
