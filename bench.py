@@ -110,6 +110,13 @@ def _prompts(n, P, V, seed):
 
 # alignment knob per pair, calibrated on B200 to alpha-hat ~0.9 at T=1 (tools/calib_alpha.py)
 PAIR_BRANCH_STD = {"llama2-7b/68m": 5e-4, "dsc-33b/1.3b": 1.7e-4, "llama3-70b/8b": 8e-5, "tiny": 2e-4}
+# SMs of the green-context partition PEARL's concurrent draft runs on (the
+# target keeps the rest; 0 = shared SMs).  A launch-bound 68M draft on 16 of
+# 148 SMs stops competing with the target's GEMMs for SM slots
+# (tools/green_sweep.sh: 7B/68M PEARL 1011 tok/s shared vs 1153 on 16 SMs;
+# the target forward is HBM-bound and no slower on 132 SMs).  Memory-bound
+# 1.3B / 8B drafts need the whole GPU.
+PAIR_DRAFT_SMS = {"llama2-7b/68m": 16, "dsc-33b/1.3b": 0, "llama3-70b/8b": 0, "tiny": 0}
 
 
 def run_gpu(args):
@@ -131,10 +138,13 @@ def run_gpu(args):
                             kappa=args.kappa)
     target, draft = llama.build_pair(args.pair, gemm_target=args.gemm_target, align=align,
                                      max_seq=args.prompt + args.new + 2 * args.gamma_max + 16, max_tokens=64,
-                                     temperature=1.0 if args.temperature <= 0 else args.temperature)
+                                     temperature=1.0 if args.temperature <= 0 else args.temperature,
+                                     draft_sms=args.draft_sms if args.draft_sms is not None
+                                     else int(os.environ.get("PEARL_DRAFT_SMS", PAIR_DRAFT_SMS[args.pair])))
     greedy = args.temperature <= 0
     temp = 1.0 if greedy else args.temperature
     V = target.cfg.vocab
+    draft_sms_used = getattr(target, "green_partition", (None, None, 0, 0))[2]
     prompts = _prompts(args.warmup + args.steps, args.prompt, V, seed=1000 + rank)
 
     def cfg_for(gamma, seed, adaptive=False):
@@ -226,6 +236,7 @@ def run_gpu(args):
             "adaptive_gamma": not args.fixed_gamma,
             "sd_gamma": args.sd_gamma, "temperature": 0.0 if greedy else temp,
             "target_gemm": args.gemm_target, "parallelism": f"replicas x{ws}",
+            "draft_sms": draft_sms_used,
             "l2": f"weights {wbytes / 1e9:.2f} GB vs 126 MB L2: "
                   + ("every forward streams HBM (no flush needed)" if wbytes > 126e6 else "L2-resident (tiny pair)"),
         },
@@ -483,6 +494,8 @@ def main():
                     help="alignment knob (default per pair, calibrated to alpha-hat ~0.9 at T=1: tools/calib_alpha.py)")
     ap.add_argument("--kappa", type=float, default=13.0)
     ap.add_argument("--gemm-target", default="tcgen05")
+    ap.add_argument("--draft-sms", type=int, default=None,
+                    help="green-context SMs for PEARL's concurrent draft (default per pair, PAIR_DRAFT_SMS)")
     ap.add_argument("--cpu-new", type=int, default=16)
     ap.add_argument("--cpu-prompt", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -386,10 +386,15 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
         _device.require_cuda()
         ds, ts = ctypes.c_void_p(), ctypes.c_void_p()
         nd, nt = ctypes.c_int(0), ctypes.c_int(0)
-        _lib.check(_lib.load().pearl_green_streams(int(draft_sms), ctypes.byref(ds), ctypes.byref(ts), ctypes.byref(nd),
-                                                   ctypes.byref(nt)), "pearl_green_streams")
-        green = (ds.value, ts.value, nd.value, nt.value)
-        target_sms = nt.value
+        rc = _lib.load().pearl_green_streams(int(draft_sms), ctypes.byref(ds), ctypes.byref(ts), ctypes.byref(nd),
+                                             ctypes.byref(nt))
+        if rc == 0:
+            green = (ds.value, ts.value, nd.value, nt.value)
+            target_sms = nt.value
+        else:  # no green contexts on this driver / device: shared SMs
+            import warnings
+            warnings.warn(f"green-context partition unavailable ({_lib.load().pearl_last_error().decode()}); "
+                          "draft and target share all SMs")
     tw, dw, tc, dc = init_pair(pair, align)
     target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature,
                         sm_count=target_sms)
