@@ -111,6 +111,15 @@ int pearl_sample_rows(int row_mode, const void* const* rows, int n_rows, int V,
                       float inv_temperature, int flags, int32_t* out_tokens,
                       int32_t* append_dst, int32_t* status, void* work, void* stream);
 
+/* pearl_sample_rows with one uniform stream per row (B independent
+ * sequences decoded in lockstep): row r draws tables[r][*cursors[r]] and
+ * advances cursors[r] by one (PEARL_F_ADVANCE).  tables / cursors are device
+ * arrays of device pointers; both may be NULL with PEARL_F_GREEDY. */
+int pearl_sample_rows_multi(int row_mode, const void* const* rows, int n_rows, int V,
+                            const double* const* tables, int n_uniforms, int32_t* const* cursors,
+                            float inv_temperature, int flags, int32_t* out_tokens, int32_t* status,
+                            void* stream);
+
 /* Device law of fp32 logits rows as float64 p1 = softmax rows (the vector a
  * SequenceModel.next_dist adapter hands to ProbDist, models.py:64-71).
  * logits: float32[n_rows, V] contiguous; out: float64[n_rows, V]. */
@@ -143,13 +152,15 @@ typedef struct {
   float norm_eps;
   int32_t sm_count;  /* SMs the model's stream-K grids span (0: all);  \
                         must match the partition it runs on            */
+  int32_t n_slots;   /* KV-cache slots (independent sequences, >= 1);   \
+                        the cache is [L, n_slots, max_seq, KV, hd]      */
 } pearl_llama_config;
 
 /* Weight / cache pointer table, in this order (all device pointers):
  *   0 embed      bf16 [V, d]          1 final_norm fp32 [d]
  *   2 lm_head    bf16 [V, d]          3 rope_cos   fp32 [max_seq, hd/2]
- *   4 rope_sin   fp32 [max_seq, hd/2] 5 k_cache    bf16 [L, max_seq, KV, hd]
- *   6 v_cache    bf16 [L, max_seq, KV, hd]
+ *   4 rope_sin   fp32 [max_seq, hd/2] 5 k_cache    bf16 [L, n_slots, max_seq, KV, hd]
+ *   6 v_cache    bf16 [L, n_slots, max_seq, KV, hd]
  *   then per layer l (base 7 + 6 l):
  *     attn_norm fp32 [d], wqkv bf16 [(H+2KV) hd, d], wo bf16 [d, H hd],
  *     mlp_norm fp32 [d], w_gate_up bf16 [2 ffn, d] (rows 2j = gate_j,
@@ -175,6 +186,18 @@ int pearl_llama_destroy(void* handle);
  * which is what makes GPU PEARL / SD greedy output token-identical to AR. */
 int pearl_llama_forward(void* handle, const int32_t* tokens, int n_tokens, int32_t* pos,
                         int flags, float* logits, void* stream);
+
+/* Batched (slot-mode) forward: token i belongs to KV slot tok_slot[i] and
+ * sits at position tok_pos[i] of that slot (device int32[n_tokens] each);
+ * K/V are appended there and fp32 logits [n_tokens, V] written for every
+ * token.  Tokens of different slots may be mixed in any order; each token's
+ * logits are bitwise the ones a single-sequence forward would produce
+ * (batch invariance), which makes a batched decode token-identical to
+ * independent per-prompt decodes.  Replaces the per-sequence next_dist
+ * calls of B independent decodes (cli.py:204-208 runs prompts as separate
+ * decodes). */
+int pearl_llama_forward_slots(void* handle, const int32_t* tokens, int n_tokens, const int32_t* tok_slot,
+                              const int32_t* tok_pos, float* logits, void* stream);
 
 size_t pearl_llama_workspace_bytes(void* handle, int n_tokens);
 

@@ -55,6 +55,7 @@ SIGNATURES = {
                                  _vp, _vp]),
     "pearl_sample_rows": (_i32, [_i32, _vp, _i32, _i32, _vp, _i32, _vp, _f32, _i32, _vp, _vp, _vp, _vp,
                                  _vp]),
+    "pearl_sample_rows_multi": (_i32, [_i32, _vp, _i32, _i32, _vp, _i32, _vp, _f32, _i32, _vp, _vp, _vp]),
     "pearl_logits_to_probs": (_i32, [_vp, _i32, _i32, _f32, _vp, _vp, _vp]),
     "pearl_residual": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp]),
     # model runtime (csrc/llama.cu)
@@ -62,6 +63,7 @@ SIGNATURES = {
     "pearl_llama_destroy": (_i32, [_vp]),
     "pearl_llama_forward": (_i32, [_vp, _vp, _i32, _vp, _i32, _vp, _vp]),
     "pearl_llama_workspace_bytes": (_sz, [_vp, _i32]),
+    "pearl_llama_forward_slots": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp, _vp]),
     "pearl_llama_profile": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp, _vp]),
     "pearl_llama_set_l2_window": (_i32, [_vp, _vp, ctypes.c_size_t, _vp]),
     "pearl_green_streams": (_i32, [_i32, _vp, _vp, _vp, _vp]),

@@ -30,6 +30,11 @@ struct EpiArgs {
   int n_kv;         // KV * hd
   int hd;
   int ld;           // leading dimension of out
+  // slot mode (batched sequences, pearl_llama_forward_slots): token t sits at
+  // position tok_pos[t] of KV slot tok_slot[t] (cache base + slot * slot_stride)
+  const int32_t* tok_pos;
+  const int32_t* tok_slot;
+  long long slot_stride;
   int32_t* adv_pos; // optional: one thread adds adv_n to *adv_pos once the kernel's
   int adv_n;        //   inputs are ready (folds the forward's position advance into
                     //   its last GEMM: every earlier reader of pos has completed)
@@ -45,6 +50,14 @@ __device__ __forceinline__ float swiglu1(float gt, float up) {
 __device__ __forceinline__ void rope2(float x0, float x1, float c, float s, float* y0, float* y1) {
   *y0 = __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, s));
   *y1 = __fadd_rn(__fmul_rn(x0, s), __fmul_rn(x1, c));
+}
+
+// Position and KV-slot offset (elements) of window token t.
+__device__ __forceinline__ int epi_pos(const EpiArgs& e, int t) {
+  return e.tok_pos ? e.tok_pos[t] : *e.pos + e.pos_add + t;
+}
+__device__ __forceinline__ size_t epi_slot_off(const EpiArgs& e, int t) {
+  return e.tok_slot ? static_cast<size_t>(e.tok_slot[t]) * static_cast<size_t>(e.slot_stride) : 0;
 }
 
 // Handle four consecutive output rows n0..n0+3 (n0 % 4 == 0) for token t.
@@ -66,7 +79,8 @@ __device__ __forceinline__ void epilogue4(const EpiArgs& e, int t, int n0, const
       break;
     }
     case EPI_QKV: {
-      const int p = *e.pos + e.pos_add + t;
+      const int p = epi_pos(e, t);
+      const size_t so = epi_slot_off(e, t);
       const int half = e.hd >> 1;
       if (n0 < e.n_q + e.n_kv) {
         float w[4];
@@ -82,11 +96,11 @@ __device__ __forceinline__ void epilogue4(const EpiArgs& e, int t, int n0, const
         } else {
           const int nk = n0 - e.n_q;
           for (int r = 0; r < 4; ++r)
-            e.kc[static_cast<size_t>(p) * e.n_kv + nk + r] = __float2bfloat16(w[r]);
+            e.kc[so + static_cast<size_t>(p) * e.n_kv + nk + r] = __float2bfloat16(w[r]);
         }
       } else {
         const int nv = n0 - e.n_q - e.n_kv;
-        for (int r = 0; r < 4; ++r) e.vc[static_cast<size_t>(p) * e.n_kv + nv + r] = __float2bfloat16(v[r]);
+        for (int r = 0; r < 4; ++r) e.vc[so + static_cast<size_t>(p) * e.n_kv + nv + r] = __float2bfloat16(v[r]);
       }
       break;
     }
@@ -150,14 +164,14 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       }
       break;
     case EPI_QKV: {
-      const int p0 = *e.pos + e.pos_add;
+      const int p0 = e.tok_pos ? 0 : *e.pos + e.pos_add;  // slot mode: per-token positions
       const int half = e.hd >> 1;
       float2 cs[MAXI], sn[MAXI];
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx < nitems && n0 < e.n_q + e.n_kv) {
-          const size_t off = static_cast<size_t>(p0 + t) * half + ((n0 % e.hd) >> 1);
+          const size_t off = static_cast<size_t>(e.tok_pos ? e.tok_pos[t] : p0 + t) * half + ((n0 % e.hd) >> 1);
           cs[i] = *reinterpret_cast<const float2*>(e.cos_t + off);
           sn[i] = *reinterpret_cast<const float2*>(e.sin_t + off);
         }
@@ -166,7 +180,8 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
-        const int p = p0 + t;
+        const int p = e.tok_pos ? e.tok_pos[t] : p0 + t;
+        const size_t so = epi_slot_off(e, t);
         float v[4];
         for (int r = 0; r < 4; ++r) v[r] = E[(g * 4 + r) * ES + t];
         if (n0 < e.n_q + e.n_kv) {
@@ -174,10 +189,10 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
           rope2(v[0], v[1], cs[i].x, sn[i].x, &w[0], &w[1]);
           rope2(v[2], v[3], cs[i].y, sn[i].y, &w[2], &w[3]);
           bf16* dst = n0 < e.n_q ? e.out_bf16 + static_cast<size_t>(t) * e.n_q + n0
-                                 : e.kc + static_cast<size_t>(p) * e.n_kv + (n0 - e.n_q);
+                                 : e.kc + so + static_cast<size_t>(p) * e.n_kv + (n0 - e.n_q);
           for (int r = 0; r < 4; ++r) dst[r] = __float2bfloat16(w[r]);
         } else {
-          bf16* dst = e.vc + static_cast<size_t>(p) * e.n_kv + (n0 - e.n_q - e.n_kv);
+          bf16* dst = e.vc + so + static_cast<size_t>(p) * e.n_kv + (n0 - e.n_q - e.n_kv);
           for (int r = 0; r < 4; ++r) dst[r] = __float2bfloat16(v[r]);
         }
       }

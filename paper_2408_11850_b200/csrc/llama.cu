@@ -399,6 +399,9 @@ struct AttnArgs {
   int pos_add, M, H, KV, hd;
   int tpb;            // window tokens per block (shares each K/V chunk load; no effect on the arithmetic)
   float scale;
+  const int32_t* tok_pos;   // slot mode (tpb == 1): per-token position and KV slot
+  const int32_t* tok_slot;
+  long long slot_stride;
 };
 
 template <int HD>
@@ -411,11 +414,16 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs 
   const int t0 = blockIdx.y * a.tpb;                  // first window token of this block
   const int MT = min(a.tpb, a.M - t0);                // tokens handled here
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p0 = *a.pos + a.pos_add + t0;             // position of the block's first token
+  const int p0 = a.tok_pos ? a.tok_pos[t0] : *a.pos + a.pos_add + t0;  // position of the block's first token
   const int ctx_max = p0 + MT;
   const int n_chunks = (ctx_max + kAttnLanesPos - 1) / kAttnLanesPos;
   const int kvh = h / (a.H / a.KV);
   const size_t kstride = static_cast<size_t>(a.KV) * HD;
+  if (a.tok_slot) {  // slot mode: this token's own sequence cache
+    const size_t so = static_cast<size_t>(a.tok_slot[t0]) * static_cast<size_t>(a.slot_stride);
+    a.kc += so;
+    a.vc += so;
+  }
   // per-warp state [M][HD + 2] in smem: o (HD), m, l
   float* st_all = reinterpret_cast<float*>(attn_smem);
   float* st = st_all + static_cast<size_t>(warp) * MT * (HD + 2);
@@ -619,7 +627,8 @@ static int stop_after() {
 
 int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_add, bool logits_all,
                   bool want_logits, float* logits, cudaStream_t st, bool use_mega, int adv_n = 0,
-                  bool* advanced = nullptr) {
+                  bool* advanced = nullptr, const int32_t* tok_slot = nullptr, const int32_t* tok_pos = nullptr) {
+  if (tok_pos) use_mega = false;
   const int abl = ablate_mask();
   const int stop = stop_after();
   int n_ops = 0;
@@ -648,11 +657,12 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   if (rc) return rc;
   g_prof.mark(OP_EMBED, st);
   if (halt()) return PEARL_OK;
-  const size_t layer_kv = static_cast<size_t>(c.max_seq) * nkv;
+  const size_t slot_kv = static_cast<size_t>(c.max_seq) * nkv;
+  const size_t layer_kv = static_cast<size_t>(std::max(1, c.n_slots)) * slot_kv;
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
   // tokens per attention block: ~2 blocks per SM, each
   // K/V chunk load shared by the block's tokens (PEARL_ATTN_TPB overrides)
-  const int tpb = attention_tpb(M, H);
+  const int tpb = tok_pos ? 1 : attention_tpb(M, H);
   const size_t attn_smem = attention_smem_bytes(tpb, hd);
   // CUDA-core (draft) models fuse every RMSNorm into the consuming GEMV
   const bool fuse_norm = c.gemm_kind == PEARL_GEMM_CUDACORE;
@@ -673,6 +683,9 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     e.sin_t = m.rope_sin;
     e.pos = pos;
     e.pos_add = pos_add;
+    e.tok_pos = tok_pos;
+    e.tok_slot = tok_slot;
+    e.slot_stride = static_cast<long long>(slot_kv);
     e.n_q = nq;
     e.n_kv = nkv;
     e.hd = hd;
@@ -681,7 +694,8 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     if (rc) return rc;
     g_prof.mark(OP_QKV, st);
   if (halt()) return PEARL_OK;
-    AttnArgs aa{m.q, e.kc, e.vc, m.o, pos, pos_add, M, H, KV, hd, tpb, scale};
+    AttnArgs aa{m.q, e.kc, e.vc, m.o, pos, pos_add, M, H, KV, hd, tpb, scale, tok_pos, tok_slot,
+                static_cast<long long>(slot_kv)};
     if (abl & 1)
       rc = PEARL_OK;
     else if (hd == 128)
@@ -765,7 +779,7 @@ int build_mega_plans(Llama& m) {
   const int G = m.tc.num_sms;
   const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads, L = c.n_layers;
   const int nq = H * hd, nkv = KV * hd;
-  const size_t layer_kv = static_cast<size_t>(c.max_seq) * nkv;
+  const size_t layer_kv = static_cast<size_t>(std::max(1, c.n_slots)) * c.max_seq * nkv;  // slot 0
   const int n_w = 4 * L + 1;
   const int Mmax = std::min(kMegaMaxTokens, c.max_tokens);
   std::vector<MegaMap> maps(static_cast<size_t>(n_w) + 4 * 16);
@@ -1054,6 +1068,27 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
   }
   if ((flags & PEARL_FWD_ADVANCE) && !advanced) {
     int rc = launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, pos, n_tokens);
+    if (rc) return rc;
+  }
+  return PEARL_OK;
+}
+
+extern "C" int pearl_llama_forward_slots(void* handle, const int32_t* tokens, int n_tokens, const int32_t* tok_slot,
+                                         const int32_t* tok_pos, float* logits, void* stream) {
+  Llama* m = static_cast<Llama*>(handle);
+  PEARL_ARG_CHECK(m && tokens && tok_slot && tok_pos && n_tokens >= 1, "bad forward_slots arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int T = m->cfg.max_tokens;
+  int32_t* pos_dummy = const_cast<int32_t*>(tok_pos);  // unread in slot mode
+  struct WindowScope {
+    explicit WindowScope(const L2Window& w) { g_l2win = w; }
+    ~WindowScope() { g_l2win = L2Window{}; }
+  } window_scope(m->l2win);
+  for (int c0 = 0; c0 < n_tokens; c0 += T) {
+    const int mt = std::min(T, n_tokens - c0);
+    int rc = forward_chunk(*m, tokens + c0, mt, pos_dummy, 0, true, logits != nullptr,
+                           logits ? logits + static_cast<size_t>(c0) * m->cfg.vocab : nullptr, st, false, 0, nullptr,
+                           tok_slot + c0, tok_pos + c0);
     if (rc) return rc;
   }
   return PEARL_OK;

@@ -462,6 +462,11 @@ struct SampleArgs {
   int32_t* append_dst;
   int32_t* status;
   WorkHdr* work;
+  // per-row streams (pearl_sample_rows_multi): row r draws tables[r][*cursors[r]]
+  // and advances its own cursor; NULL for the shared-stream form
+  const double* const* tables;
+  int32_t* const* cursors;
+  int multi;  // pearl_sample_rows_multi launch: no shared cursor / arrival counter
 };
 
 __global__ void __launch_bounds__(kThreads) sample_rows_kernel(SampleArgs A) {
@@ -476,7 +481,9 @@ __global__ void __launch_bounds__(kThreads) sample_rows_kernel(SampleArgs A) {
   PEARL_TR(1);
   const int lo = plan[3];
   const bool greedy = (A.flags & PEARL_F_GREEDY) != 0;
-  const int cur = A.cursor ? *A.cursor : 0;
+  const bool per_row = A.tables != nullptr;
+  const int cur = per_row ? *A.cursors[row] - row : (A.cursor ? *A.cursor : 0);  // (row r reads cur + r)
+  const double* table = per_row ? A.tables[row] : A.uniforms;
   const void* rows[1] = {A.rows[row]};
   double* sl[1] = {P};
   RowNorm nm[1];
@@ -489,7 +496,7 @@ __global__ void __launch_bounds__(kThreads) sample_rows_kernel(SampleArgs A) {
       st = PEARL_ERR_VALUE;
     } else {
       tok = cluster_search(cc, s, plan, A.job.V, [&](int i) { return P[i - lo]; },
-                           A.uniforms[cur + row], nullptr);
+                           table[cur + row], nullptr);
     }
   }
   PEARL_TR(20);
@@ -499,6 +506,10 @@ __global__ void __launch_bounds__(kThreads) sample_rows_kernel(SampleArgs A) {
   A.out[row] = tok;
   if (row == 0 && A.append_dst) *A.append_dst = tok;
   if (st != PEARL_OK && A.status) atomicMax(A.status, st);
+  if (A.multi) {
+    if (per_row && (A.flags & PEARL_F_ADVANCE) && !greedy && st == PEARL_OK) *A.cursors[row] = cur + row + 1;
+    return;
+  }
   __threadfence();
   const int old = atomicAdd(&A.work->arrived, 1);
   if (old == A.n_rows - 1) {
@@ -707,6 +718,31 @@ extern "C" int pearl_sample_rows(int row_mode, const void* const* rows, int n_ro
   a.append_dst = append_dst;
   a.status = status;
   a.work = static_cast<WorkHdr*>(work);
+  return launch_clustered(sample_rows_kernel, n_rows, plan->C, smem_bytes(*plan, 1), stream, a);
+}
+
+extern "C" int pearl_sample_rows_multi(int row_mode, const void* const* rows, int n_rows, int V,
+                                       const double* const* tables, int n_uniforms, int32_t* const* cursors,
+                                       float inv_temperature, int flags, int32_t* out_tokens, int32_t* status,
+                                       void* stream) {
+  PEARL_ARG_CHECK(n_rows >= 1, "need at least one row");
+  PEARL_ARG_CHECK(rows && out_tokens && ((flags & PEARL_F_GREEDY) || (tables && cursors)), "null argument");
+  PEARL_ARG_CHECK(inv_temperature > 0.0f, "inverse temperature must be positive");
+  int st = configure_all();
+  if (st != PEARL_OK) return st;
+  const VocabPlan* plan = get_plan(V);
+  if (!plan) return PEARL_ERR_ARG;
+  SampleArgs a{};
+  a.job = RowJob{row_mode, inv_temperature, V, plan->d_plan, plan->cap};
+  a.flags = flags;
+  a.n_rows = n_rows;
+  a.rows = rows;
+  a.n_uniforms = n_uniforms;
+  a.out = out_tokens;
+  a.status = status;
+  a.tables = (flags & PEARL_F_GREEDY) ? nullptr : tables;
+  a.cursors = (flags & PEARL_F_GREEDY) ? nullptr : cursors;
+  a.multi = 1;
   return launch_clustered(sample_rows_kernel, n_rows, plan->C, smem_bytes(*plan, 1), stream, a);
 }
 

@@ -180,7 +180,7 @@ def init_pair(pair: str, align: AlignSpec = AlignSpec(), device=None):
 class _CConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "ffn",
                                               "vocab", "max_seq", "max_tokens", "gemm_kind")] + [
-        ("norm_eps", ctypes.c_float), ("sm_count", ctypes.c_int32)]
+        ("norm_eps", ctypes.c_float), ("sm_count", ctypes.c_int32), ("n_slots", ctypes.c_int32)]
 
 
 GEMM_KINDS = {"cudacore": 0, "tcgen05": 1}
@@ -213,7 +213,8 @@ class LlamaModel(SequenceModel):
 
     def __init__(self, cfg: LlamaConfig, weights: Dict[str, object], gemm: str = "cudacore",
                  max_seq: int = 1024, max_tokens: int = 64, temperature: float = 1.0, bos_id: int = 1,
-                 latency: Optional[LatencyProfile] = None, l2_resident: bool = False, sm_count: int = 0):
+                 latency: Optional[LatencyProfile] = None, l2_resident: bool = False, sm_count: int = 0,
+                 n_slots: int = 1):
         self.device = _device.require_cuda()
         self.cfg = cfg
         self.vocab_size = cfg.vocab
@@ -229,7 +230,10 @@ class LlamaModel(SequenceModel):
         cos, sin = rope_tables(hd, max_seq, cfg.rope_theta)
         self.rope_cos = torch.from_numpy(cos).to(self.device)
         self.rope_sin = torch.from_numpy(sin).to(self.device)
-        kv_shape = (cfg.n_layers, max_seq, cfg.n_kv_heads, hd)
+        # KV cache [L, slots, max_seq, KV, hd]: slot 0 serves the single-sequence
+        # engines, slots 0..n_slots-1 the batched ones (batched.py)
+        self.n_slots = int(n_slots)
+        kv_shape = (cfg.n_layers, self.n_slots, max_seq, cfg.n_kv_heads, hd)
         self.k_cache = torch.zeros(kv_shape, dtype=torch.bfloat16, device=self.device)
         self.v_cache = torch.zeros(kv_shape, dtype=torch.bfloat16, device=self.device)
         ptrs = [weights["embed"], weights["final_norm"], weights["lm_head"], self.rope_cos, self.rope_sin,
@@ -240,7 +244,7 @@ class LlamaModel(SequenceModel):
             assert t.is_cuda and t.is_contiguous()
         self._ptr_arr = (ctypes.c_void_p * len(ptrs))(*[t.data_ptr() for t in ptrs])
         c = _CConfig(cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.n_kv_heads, hd, cfg.ffn, cfg.vocab, max_seq,
-                     max_tokens, GEMM_KINDS[gemm], cfg.norm_eps, int(sm_count))
+                     max_tokens, GEMM_KINDS[gemm], cfg.norm_eps, int(sm_count), self.n_slots)
         h = ctypes.c_void_p()
         _lib.check(_lib.load().pearl_llama_create(ctypes.byref(c), self._ptr_arr, len(ptrs), ctypes.byref(h)),
                    "pearl_llama_create")
@@ -264,6 +268,13 @@ class LlamaModel(SequenceModel):
         _lib.check(_lib.load().pearl_llama_forward(self.handle, _device.ptr(tokens), int(n), _device.ptr(pos),
                                                    int(flags), _device.ptr(logits), _device.stream_ptr(stream)),
                    "pearl_llama_forward")
+
+    def forward_slots(self, tokens: torch.Tensor, n: int, tok_slot: torch.Tensor, tok_pos: torch.Tensor,
+                      logits: Optional[torch.Tensor], stream=None) -> None:
+        """Batched forward: token i at position tok_pos[i] of KV slot tok_slot[i] (device int32)."""
+        _lib.check(_lib.load().pearl_llama_forward_slots(self.handle, _device.ptr(tokens), int(n), _device.ptr(tok_slot),
+                                                         _device.ptr(tok_pos), _device.ptr(logits),
+                                                         _device.stream_ptr(stream)), "pearl_llama_forward_slots")
 
     def forward_logits(self, tokens: Sequence[int], start: int = 0) -> torch.Tensor:
         """fp32 logits of every token of ``tokens`` placed at positions start.. (fresh cache)."""
@@ -363,7 +374,8 @@ def inv_temp(t: float) -> float:
 
 def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: str = "auto",
                align: AlignSpec = AlignSpec(), max_seq: int = 1024, max_tokens: int = 64,
-               temperature: float = 1.0, l2_draft: Optional[bool] = None, draft_sms: Optional[int] = None):
+               temperature: float = 1.0, l2_draft: Optional[bool] = None, draft_sms: Optional[int] = None,
+               n_slots: int = 1):
     """(target LlamaModel, draft LlamaModel) with controlled-alignment random weights.
 
     ``l2_draft``: keep the draft's streamed weights in persisting L2
@@ -397,11 +409,11 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
                           "draft and target share all SMs")
     tw, dw, tc, dc = init_pair(pair, align)
     target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature,
-                        sm_count=target_sms)
+                        sm_count=target_sms, n_slots=n_slots)
     if gemm_draft == "auto":
         gemm_draft = "tcgen05" if dc.weight_bytes() > 1e9 else "cudacore"
     draft = LlamaModel(dc, dw, gemm=gemm_draft, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature,
-                       l2_resident=l2_draft)
+                       l2_resident=l2_draft, n_slots=n_slots)
     if green is not None:
         target.green_partition = green  # (draft stream, target stream, draft SMs, target SMs)
     return target, draft
