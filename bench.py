@@ -136,7 +136,9 @@ def run_gpu(args):
 
     align = llama.AlignSpec(branch_std=args.branch_std if args.branch_std is not None else PAIR_BRANCH_STD[args.pair],
                             kappa=args.kappa)
+    sweep_bs = [int(b) for b in args.batch_sweep.split(",") if b] if args.batch_sweep else []
     target, draft = llama.build_pair(args.pair, gemm_target=args.gemm_target, align=align,
+                                     n_slots=max([1] + sweep_bs),
                                      max_seq=args.prompt + args.new + 2 * args.gamma_max + 16, max_tokens=64,
                                      temperature=1.0 if args.temperature <= 0 else args.temperature,
                                      draft_sms=args.draft_sms if args.draft_sms is not None
@@ -197,6 +199,7 @@ def run_gpu(args):
     # roofline of the dominant kernel sequence: one target window forward
     rl = roofline(target, draft, args.gamma, args)
     target_bytes, draft_bytes = target.cfg.weight_bytes(), draft.cfg.weight_bytes()
+    sweep = batch_sweep(target, draft, args, sweep_bs, greedy, temp, ws) if sweep_bs else None
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(target, draft, prompts[0], args, greedy, temp)
@@ -260,6 +263,7 @@ def run_gpu(args):
         "exact_cdf_fallbacks": int(results["pearl"]["fallbacks"]),
         "roofline": rl,
         "split_pair": split,
+        "batch_sweep": sweep,
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
@@ -268,6 +272,38 @@ def run_gpu(args):
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def batch_sweep(target, draft, args, bs, greedy, temp, ws):
+    """C5: B prompts decoded in lockstep (batched.py) by PEARL, SD and AR at
+    fixed gamma; tokens/s of the whole batch (device time, per rank; the
+    whole-job figure multiplies by the ranks, which decode disjoint batches)."""
+    import torch
+    import paper_2408_11850_b200 as pk
+    from paper_2408_11850_b200 import batched
+    out = {}
+    V = target.cfg.vocab
+    for B in bs:
+        prompts = _prompts(B, args.prompt, V, seed=3000 + B)
+        cfg = pk.EngineConfig(gamma=args.gamma, max_new_tokens=args.new, seed=29, greedy=greedy, temperature=temp)
+        row = {}
+        for kind, fn in (("pearl", lambda: batched.decode_pearl_batch(draft, target, prompts, cfg)),
+                         ("sd", lambda: batched.decode_sd_batch(draft, target, prompts, cfg)),
+                         ("ar", lambda: batched.decode_autoregressive_batch(target, prompts, cfg))):
+            fn()  # warm-up
+            torch.cuda.synchronize()
+            res = fn()
+            toks = sum(len(r.tokens) for r in res)
+            dev_s = res[0].stats["device_s"]
+            row[kind] = round(ws * toks / dev_s, 2)
+            if kind != "ar":
+                steps = [st for r in res for st in r.steps]
+                row[kind + "_alpha_hat"] = round(pk.empirical_acceptance(steps), 4)
+        row["pearl_vs_ar"] = round(row["pearl"] / row["ar"], 3)
+        row["pearl_vs_sd"] = round(row["pearl"] / row["sd"], 3)
+        out[str(B)] = row
+    return {"unit": "tokens/s (whole batch, all ranks)", "gamma": args.gamma, "by_batch": out,
+            "note": "host-driven lockstep loop (no CUDA graphs yet); fixed gamma"}
 
 
 def split_leg(args, ws, rank, greedy, temp, ar_agg):
@@ -500,6 +536,8 @@ def main():
     ap.add_argument("--cpu-prompt", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-split", action="store_true", help="N>=2: skip the split-pair (draft GPU / target GPU) leg")
+    ap.add_argument("--batch-sweep", default="1,4,16",
+                    help="C5: comma-separated batch sizes decoded in lockstep (empty string: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
