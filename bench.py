@@ -139,7 +139,7 @@ def run_gpu(args):
     sweep_bs = [int(b) for b in args.batch_sweep.split(",") if b] if args.batch_sweep else []
     target, draft = llama.build_pair(args.pair, gemm_target=args.gemm_target, align=align,
                                      n_slots=max([1] + sweep_bs),
-                                     max_seq=args.prompt + args.new + 2 * args.gamma_max + 16, max_tokens=64,
+                                     max_seq=args.prompt + args.new + 2 * args.gamma_max + 16, max_tokens=128,
                                      temperature=1.0 if args.temperature <= 0 else args.temperature,
                                      draft_sms=args.draft_sms if args.draft_sms is not None
                                      else int(os.environ.get("PEARL_DRAFT_SMS", PAIR_DRAFT_SMS[args.pair])))

@@ -14,7 +14,7 @@ constexpr int kMegaMaxTokens = 16;   // window sizes served by the persistent fo
 constexpr int kMegaTileN = 128;      // == kTileN  (tc_common.cuh)
 constexpr int kMegaTileK = 64;       // == kTileK
 constexpr int kMegaCtrStride = 32;  // words between phase counters (one 128 B line each)
-constexpr int kMegaPartialTok = 64;  // == kMaxTokTiles * kTokTile (partials row pitch bound)
+constexpr int kMegaPartialTok = 128;  // == kMaxTokTiles * kTokTile (partials row pitch bound)
 
 enum MegaKind { MG_EMBED = 0, MG_NORM = 1, MG_GEMM = 2, MG_ATTN = 3 };
 

@@ -44,6 +44,12 @@ struct TcArgs {
   float* partials;
   int* flags;
   int l2_prefetch;  // W tiles past the ring requested into L2 before the PDL wait
+  // the NEXT GEMM of the forward (weights [nN, nK]): once this CTA's producer
+  // has issued its last load, warp 0 requests the first next_pf k-blocks the
+  // same CTA index will stream there into L2 (plain bulk prefetches, one per
+  // weight row run), so HBM keeps streaming through this kernel's tail
+  const __nv_bfloat16* nW;
+  int nN, nK, nG, next_pf;
 };
 
 // ---- kernel ------------------------------------------------------------------
@@ -135,6 +141,30 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
       }
     }
+    __syncwarp();
+    if (a.next_pf > 0 && a.nW != nullptr) {
+      const int nKB = (a.nK + kTileK - 1) / kTileK;
+      const long long nT = static_cast<long long>((a.nN + kTileN - 1) / kTileN) * nKB;
+      if (blockIdx.x < a.nG) {
+        const long long q0 = static_cast<long long>(blockIdx.x) * nT / a.nG;
+        const long long q1 = min(static_cast<long long>(blockIdx.x + 1) * nT / a.nG, q0 + a.next_pf);
+        // runs of consecutive k-blocks inside one tile: rows x contiguous bytes
+        for (long long x = q0; x < q1;) {
+          const int tile = static_cast<int>(x / nKB), kb = static_cast<int>(x % nKB);
+          const int len = static_cast<int>(min(q1 - x, static_cast<long long>(nKB - kb)));
+          const int kc = kb * kTileK, kn = min(len * kTileK, a.nK - kc);
+          const uint32_t bytes = static_cast<uint32_t>(kn) * 2u;
+          for (int r = lane; r < kTileN; r += 32) {
+            const int row = tile * kTileN + r;
+            if (row < a.nN && (bytes & 15u) == 0)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.nW + static_cast<size_t>(row) * a.nK + kc),
+                           "r"(bytes)
+                           : "memory");
+          }
+          x += len;
+        }
+      }
+    }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---- MMA issuer: one accumulator per unit (run of k-blocks inside a tile)
@@ -152,12 +182,14 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           unsigned char* st = smem + s * stage_bytes;
           const uint64_t adesc = umma_desc_sw128(st);
-          for (int j = 0; j < NT; ++j) {
-            const uint64_t bdesc = umma_desc_sw128(st + kWBytes + j * kXBytes);
+          // all NT token tiles in ONE MMA of N = 16 NT columns (the tiles are
+          // contiguous rows of one SW128 operand); per-column arithmetic is the
+          // same for any N (tests/test_gemm_gpu.py::test_batch_invariance)
+          const uint64_t bdesc = umma_desc_sw128(st + kWBytes);
 #pragma unroll
-            for (int kk = 0; kk < kTileK / 16; ++kk)
-              umma_bf16(acc + j * kTokTile, adesc + 2 * kk, bdesc + 2 * kk, (kb > u.kb0 || kk > 0) ? 1u : 0u);
-          }
+          for (int kk = 0; kk < kTileK / 16; ++kk)
+            umma_bf16_n(acc, adesc + 2 * kk, bdesc + 2 * kk, (kb > u.kb0 || kk > 0) ? 1u : 0u,
+                        umma_idesc(NT * kTokTile));
           umma_commit(&empty[s]);
         }
         umma_commit(&acc_full[b]);
@@ -209,7 +241,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         const float* src = a.partials + (static_cast<size_t>(tile) * a.seg_max * kTileN + row) * Mp;
         const size_t sstride = static_cast<size_t>(kTileN) * Mp;
         constexpr int NQ = NT * 4;          // token quads per row (max)
-        constexpr int SB = 16 / NQ;         // splits per batch
+        constexpr int SB = NQ >= 16 ? 1 : 16 / NQ;  // splits per batch
         const int nq = Mp / 4;
         float4 acc[NQ];
 #pragma unroll
@@ -253,6 +285,9 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
 // W tiles per CTA requested into L2 ahead of the ring before the PDL wait
 // (PEARL_L2PF overrides).
 constexpr int kDefaultL2Prefetch = 0;
+// k-blocks of the next GEMM per CTA requested into L2 in this GEMM's tail
+// (PEARL_NEXTPF overrides).
+constexpr int kDefaultNextPrefetch = 0;
 
 namespace {
 
@@ -355,6 +390,10 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
     if (e == cudaSuccess) e = set_attr<2>();
     if (e == cudaSuccess) e = set_attr<3>();
     if (e == cudaSuccess) e = set_attr<4>();
+    if (e == cudaSuccess) e = set_attr<5>();
+    if (e == cudaSuccess) e = set_attr<6>();
+    if (e == cudaSuccess) e = set_attr<7>();
+    if (e == cudaSuccess) e = set_attr<8>();
     g_attr_err = e;
   });
   PEARL_CUDA_TRY(g_attr_err);
@@ -362,6 +401,8 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   {
     const char* v = std::getenv("PEARL_L2PF");
     ctx.l2_prefetch_iters = v ? std::max(0, std::atoi(v)) : kDefaultL2Prefetch;
+    const char* w = std::getenv("PEARL_NEXTPF");
+    ctx.next_prefetch_iters = w ? std::max(0, std::atoi(w)) : kDefaultNextPrefetch;
   }
   const int hd = c.head_dim;
   const int shapes[5][2] = {{(c.n_heads + 2 * c.n_kv_heads) * hd, c.d_model},
@@ -395,7 +436,7 @@ void tc_free(TcGemmCtx& ctx) {
 }
 
 int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int M, int N, int K, const EpiArgs& e,
-            cudaStream_t st, int force_splits) {
+            cudaStream_t st, int force_splits, TcNext next) {
   if (M < 1 || M > kMaxTokTiles * kTokTile) {
     set_error("tc_gemm: M must be in [1, 64]");
     return PEARL_ERR_ARG;
@@ -428,6 +469,13 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;
   a.l2_prefetch = ctx.l2_prefetch_iters;
+  a.nW = next.W;
+  a.nN = next.N;
+  a.nK = next.K;
+  a.nG = next.W ? static_cast<int>(std::min<long long>(ctx.num_sms, static_cast<long long>((next.N + kTileN - 1) / kTileN) *
+                                                                      ((next.K + kTileK - 1) / kTileK)))
+                : 0;
+  a.next_pf = ctx.next_prefetch_iters;
   if (static_cast<size_t>(tiles) * a.seg_max * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
       tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");
@@ -456,9 +504,25 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
       cfg.dynamicSmemBytes = TcCfg<3>::kSmem;
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<3>, it->second.map, xmap, a));
       break;
-    default:
+    case 4:
       cfg.dynamicSmemBytes = TcCfg<4>::kSmem;
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<4>, it->second.map, xmap, a));
+      break;
+    case 5:
+      cfg.dynamicSmemBytes = TcCfg<5>::kSmem;
+      PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<5>, it->second.map, xmap, a));
+      break;
+    case 6:
+      cfg.dynamicSmemBytes = TcCfg<6>::kSmem;
+      PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<6>, it->second.map, xmap, a));
+      break;
+    case 7:
+      cfg.dynamicSmemBytes = TcCfg<7>::kSmem;
+      PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<7>, it->second.map, xmap, a));
+      break;
+    default:
+      cfg.dynamicSmemBytes = TcCfg<8>::kSmem;
+      PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<8>, it->second.map, xmap, a));
       break;
   }
   count_launch();

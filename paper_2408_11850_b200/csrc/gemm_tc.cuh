@@ -34,6 +34,7 @@ struct TcGemmCtx {
   int max_tokens = 0;
   int num_sms = 148;
   int min_plan_splits = 1;
+  int next_prefetch_iters = 0;  // k-blocks of the NEXT GEMM per CTA prefetched into L2 in the tail
   int l2_prefetch_iters = 0;  // next-GEMM weight tiles per CTA requested into L2 (0: off)  // workspace sized for at least this many splits (microbenchmarks)
   // per weight matrix, keyed by (address, N, K): a map encodes the shape too
   std::map<std::tuple<const void*, int, int>, TcWeightMap> wmaps;
@@ -41,8 +42,14 @@ struct TcGemmCtx {
 
 int tc_init(TcGemmCtx& ctx, const pearl_llama_config& cfg);
 void tc_free(TcGemmCtx& ctx);
+// The GEMM that follows in the forward (its weights are prefetched into L2
+// during this GEMM's tail; W == nullptr: none).
+struct TcNext {
+  const __nv_bfloat16* W = nullptr;
+  int N = 0, K = 0;
+};
 int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int M, int N, int K,
-            const EpiArgs& e, cudaStream_t st, int force_grid = 0);
+            const EpiArgs& e, cudaStream_t st, int force_grid = 0, TcNext next = TcNext{});
 // number of K splits the (legacy round-robin) planner picks for an (N, K) GEMM
 int tc_splits(int N, int K, int num_sms);
 // most stream-K segments any tile of an (tiles x KB) GEMM is cut into over G CTAs

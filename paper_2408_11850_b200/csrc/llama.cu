@@ -576,9 +576,9 @@ int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs
 
 static int ablate_mask();
 int launch_gemm(Llama& m, const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
-                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
+                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}, TcNext next = TcNext{}) {
   if (ablate_mask() & 4) return PEARL_OK;
-  if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st);
+  if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st, 0, next);
   return launch_gemv(W, X, M, N, K, e, st, nrm);
 }
 
@@ -690,7 +690,8 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     e.n_kv = nkv;
     e.hd = hd;
     rc = launch_gemm(m, L.wqkv, m.x, M, nq + 2 * nkv, d, e, st,
-                     fuse_norm ? GemvNorm{m.h, L.attn_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
+                     fuse_norm ? GemvNorm{m.h, L.attn_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f},
+                     TcNext{L.wo, d, nq});
     if (rc) return rc;
     g_prof.mark(OP_QKV, st);
   if (halt()) return PEARL_OK;
@@ -711,7 +712,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     r.kind = EPI_RESID;
     r.out_f32 = m.h;
     r.ld = d;
-    rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
+    rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st, GemvNorm{nullptr, nullptr, 0.f}, TcNext{L.wgu, 2 * c.ffn, d});
     if (rc) return rc;
     g_prof.mark(OP_O, st);
   if (halt()) return PEARL_OK;
@@ -726,11 +727,14 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     g.out_bf16 = m.act;
     g.ld = c.ffn;
     rc = launch_gemm(m, L.wgu, m.x, M, 2 * c.ffn, d, g, st,
-                     fuse_norm ? GemvNorm{m.h, L.mlp_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
+                     fuse_norm ? GemvNorm{m.h, L.mlp_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f},
+                     TcNext{L.wdown, d, c.ffn});
     if (rc) return rc;
     g_prof.mark(OP_GU, st);
   if (halt()) return PEARL_OK;
-    rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r, st);
+    const TcNext after_down = l + 1 < c.n_layers ? TcNext{m.layers[l + 1].wqkv, nq + 2 * nkv, d}
+                              : (want_logits ? TcNext{m.lm_head, c.vocab, d} : TcNext{});
+    rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r, st, GemvNorm{nullptr, nullptr, 0.f}, after_down);
     if (rc) return rc;
     g_prof.mark(OP_DOWN, st);
   if (halt()) return PEARL_OK;
@@ -933,7 +937,8 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   PEARL_ARG_CHECK(c.d_model <= 4 * kNormThreads * kNormVec, "d_model too large for the norm kernel");
   PEARL_ARG_CHECK(c.gemm_kind != PEARL_GEMM_CUDACORE || (c.max_tokens <= kGemvMaxNormTok && c.d_model % 256 == 0),
                   "CUDA-core models need max_tokens <= 64 and d_model % 256 == 0 (fused norm)");
-  PEARL_ARG_CHECK(c.max_tokens >= 1 && c.max_tokens <= 64, "max_tokens in [1, 64]");
+  PEARL_ARG_CHECK(c.max_tokens >= 1 && c.max_tokens <= (c.gemm_kind == PEARL_GEMM_TCGEN05 ? 128 : 64),
+                  "max_tokens in [1, 128] (tcgen05) / [1, 64] (CUDA-core)");
   PEARL_ARG_CHECK(c.max_seq >= 1 && c.max_seq <= 4096, "max_seq in [1, 4096]");
   Llama* m = new Llama();
   m->cfg = c;
@@ -1024,7 +1029,7 @@ extern "C" int pearl_gemm(int kind, const void* W, const void* X, float* Y, int 
     c.head_dim = 128;
     c.ffn = 28672;
     c.vocab = 131072;
-    c.max_tokens = 64;
+    c.max_tokens = 128;
     g_gemm_ctx.min_plan_splits = 16;
     int rc = tc_init(g_gemm_ctx, c);
     if (rc) return rc;

@@ -14,7 +14,7 @@ namespace pearl {
 constexpr int kTileN = 128;    // weight rows per tile (MMA-M)
 constexpr int kTileK = 64;     // K per stage (one 128-byte swizzle row)
 constexpr int kTokTile = 16;   // tokens per MMA (MMA-N)
-constexpr int kMaxTokTiles = 4;
+constexpr int kMaxTokTiles = 8;  // windows / batched passes up to 128 tokens
 constexpr int kWBytes = kTileN * kTileK * 2;   // 16 KB
 constexpr int kXBytes = kTokTile * kTileK * 2; // 2 KB per token tile
 constexpr int kMaxStages = 8;
@@ -105,6 +105,21 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t 
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+// Same MMA with N = n columns (n % 16 == 0, <= 256): the NT token tiles of a
+// stage are one contiguous K-major SW128 operand of n rows.
+__host__ __device__ constexpr uint32_t umma_idesc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((static_cast<uint32_t>(n) >> 3) << 17) | ((kTileN >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16_n(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate,
+                                            uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {

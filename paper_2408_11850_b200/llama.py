@@ -408,11 +408,14 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
             warnings.warn(f"green-context partition unavailable ({_lib.load().pearl_last_error().decode()}); "
                           "draft and target share all SMs")
     tw, dw, tc, dc = init_pair(pair, align)
-    target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature,
-                        sm_count=target_sms, n_slots=n_slots)
+    target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq,
+                        max_tokens=max_tokens if gemm_target == "tcgen05" else min(max_tokens, 64),
+                        temperature=temperature, sm_count=target_sms, n_slots=n_slots)
     if gemm_draft == "auto":
         gemm_draft = "tcgen05" if dc.weight_bytes() > 1e9 else "cudacore"
-    draft = LlamaModel(dc, dw, gemm=gemm_draft, max_seq=max_seq, max_tokens=max_tokens, temperature=temperature,
+    # the CUDA-core engine's fused-norm prologue takes <= 64 tokens per pass
+    draft_tokens = max_tokens if gemm_draft == "tcgen05" else min(max_tokens, 64)
+    draft = LlamaModel(dc, dw, gemm=gemm_draft, max_seq=max_seq, max_tokens=draft_tokens, temperature=temperature,
                        l2_resident=l2_draft, n_slots=n_slots)
     if green is not None:
         target.green_partition = green  # (draft stream, target stream, draft SMs, target SMs)

@@ -33,7 +33,7 @@ def _gemm(lib, kind, W, X, splits=0):
 def test_matches_fp32_reference(lib, kind, N, K):
     g = torch.Generator(device="cuda").manual_seed(N * 7 + K)
     W = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
-    for M in (1, 3, 16, 17, 40, 64):
+    for M in (1, 3, 16, 17, 40, 64, 100, 128):
         X = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
         Y = _gemm(lib, kind, W, X)
         ref = X.float() @ W.float().T
@@ -47,9 +47,9 @@ def test_batch_invariance(lib, kind):
     g = torch.Generator(device="cuda").manual_seed(5)
     for N, K in [(4096, 4096), (300, 1376), (32000, 768)]:
         W = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
-        X = torch.randn(64, K, generator=g, device="cuda").to(torch.bfloat16)
+        X = torch.randn(128, K, generator=g, device="cuda").to(torch.bfloat16)
         full = _gemm(lib, kind, W, X)
-        for M in (1, 2, 5, 16, 33):
+        for M in (1, 2, 5, 16, 33, 64, 100):
             part = _gemm(lib, kind, W, X[:M].contiguous())
             assert torch.equal(part, full[:M]), (kind, N, K, M)
         # a token's row does not depend on the other rows' values either
