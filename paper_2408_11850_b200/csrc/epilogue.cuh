@@ -109,12 +109,20 @@ __device__ __forceinline__ void epilogue4(const EpiArgs& e, int t, int n0, const
 
 // Epilogue of one 128-row output tile for tokens 0..M-1 on the tcgen05 paths
 // (per-GEMM kernel and persistent forward): E is the tile's fp32 result in
-// smem, E[row * ES + t]; 128 threads (et) take items (4-row group g, token
-// t) = (idx % 32, idx / 32), idx = et + 128 i.  Same arithmetic as epilogue4,
-// but every global load of all of a thread's items (residual rows, RoPE
-// tables, the position) is issued before any store, so a tile's epilogue
-// costs one memory round trip instead of one per item.
-template <int MAXI>
+// smem -- row-major E[row * ES + t] (TR = false, persistent forward) or
+// token-major E[t * ES + row] (TR = true, per-GEMM kernel: conflict-free
+// staging stores and one 16-byte read per item); 128 threads (et) take items
+// (4-row group g, token t) = (idx % 32, idx / 32), idx = et + 128 i.  Same
+// arithmetic as epilogue4, but every global load of all of a thread's items
+// (residual rows, RoPE tables, the position) is issued before any store, so a
+// tile's epilogue costs one memory round trip instead of one per item.
+template <bool TR>
+__device__ __forceinline__ float4 epi_rows4(const float* E, int ES, int g, int t) {
+  if (TR) return *reinterpret_cast<const float4*>(E + t * ES + g * 4);
+  return make_float4(E[(g * 4) * ES + t], E[(g * 4 + 1) * ES + t], E[(g * 4 + 2) * ES + t], E[(g * 4 + 3) * ES + t]);
+}
+
+template <int MAXI, bool TR = false>
 __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const float* E, int ES, int M, int N,
                                               int et) {
   constexpr int kGroups = 32;  // 128 rows / 4
@@ -126,8 +134,14 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
         float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
-        for (int r = 0; r < 4; ++r)
-          if (n0 + r < N) o[r] = E[(g * 4 + r) * ES + t];
+        const float4 v = epi_rows4<TR>(E, ES, g, t);
+        if (n0 + 3 < N && (e.ld & 3) == 0) {
+          *reinterpret_cast<float4*>(o) = v;
+        } else {
+          const float w[4] = {v.x, v.y, v.z, v.w};
+          for (int r = 0; r < 4; ++r)
+            if (n0 + r < N) o[r] = w[r];
+        }
       }
       break;
     case EPI_RESID: {
@@ -143,12 +157,13 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
         float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
+        const float4 v = epi_rows4<TR>(E, ES, g, t);
         if (n0 + 3 < N) {
-          *reinterpret_cast<float4*>(o) = make_float4(hv[i].x + E[(g * 4) * ES + t], hv[i].y + E[(g * 4 + 1) * ES + t],
-                                                      hv[i].z + E[(g * 4 + 2) * ES + t], hv[i].w + E[(g * 4 + 3) * ES + t]);
+          *reinterpret_cast<float4*>(o) = make_float4(hv[i].x + v.x, hv[i].y + v.y, hv[i].z + v.z, hv[i].w + v.w);
         } else {
+          const float w[4] = {v.x, v.y, v.z, v.w};
           for (int r = 0; r < 4; ++r)
-            if (n0 + r < N) o[r] += E[(g * 4 + r) * ES + t];
+            if (n0 + r < N) o[r] += w[r];
         }
       }
       break;
@@ -158,9 +173,9 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
-        for (int r = 0; r < 4; r += 2)
-          e.out_bf16[static_cast<size_t>(t) * e.ld + (n0 + r) / 2] =
-              __float2bfloat16(swiglu1(E[(g * 4 + r) * ES + t], E[(g * 4 + r + 1) * ES + t]));
+        const float4 v = epi_rows4<TR>(E, ES, g, t);
+        e.out_bf16[static_cast<size_t>(t) * e.ld + n0 / 2] = __float2bfloat16(swiglu1(v.x, v.y));
+        e.out_bf16[static_cast<size_t>(t) * e.ld + (n0 + 2) / 2] = __float2bfloat16(swiglu1(v.z, v.w));
       }
       break;
     case EPI_QKV: {
@@ -182,8 +197,8 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
         if (idx >= nitems || n0 >= N) continue;
         const int p = e.tok_pos ? e.tok_pos[t] : p0 + t;
         const size_t so = epi_slot_off(e, t);
-        float v[4];
-        for (int r = 0; r < 4; ++r) v[r] = E[(g * 4 + r) * ES + t];
+        const float4 v4 = epi_rows4<TR>(E, ES, g, t);
+        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
         if (n0 < e.n_q + e.n_kv) {
           float w[4];
           rope2(v[0], v[1], cs[i].x, sn[i].x, &w[0], &w[1]);

@@ -216,16 +216,15 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&acc_empty[b]);  // the MMA warp may reuse this accumulator
       if (u.nseg == 1) {
+        // token-major staging: a warp's 32 rows of one token are 128 contiguous bytes
 #pragma unroll
-        for (int q = 0; q < NT * 4; ++q)
-          *reinterpret_cast<float4*>(E + row * ES + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int c = 0; c < NT * 16; ++c) E[c * ES + row] = v[c];
       } else {
-        // this split's fp32 partial row: Mp contiguous floats (float4 stores)
-        float* dst = a.partials + ((static_cast<size_t>(tile) * a.seg_max + u.seg) * kTileN + row) * Mp;
+        // this split's fp32 partial tile, token-major [t][row]: coalesced
+        float* dst = a.partials + (static_cast<size_t>(tile) * a.seg_max + u.seg) * Mp * kTileN + row;
 #pragma unroll
-        for (int q = 0; q < NT * 4; ++q)
-          if (4 * q < Mp)
-            *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int c = 0; c < NT * 16; ++c)
+          if (c < a.M) dst[static_cast<size_t>(c) * kTileN] = v[c];
         epi_bar();  // all partial stores of the CTA precede the releasing atomic
         if (et == 0) {
           int old;
@@ -235,43 +234,32 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         epi_bar();
         if (!*s_last) continue;
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        // Fixed split order => independent of arrival order and of M.  Each
-        // thread owns one row; loads of up to 16 (split, token-quad) float4
-        // are in flight together, then summed per quad in split order.
-        const float* src = a.partials + (static_cast<size_t>(tile) * a.seg_max * kTileN + row) * Mp;
-        const size_t sstride = static_cast<size_t>(kTileN) * Mp;
-        constexpr int NQ = NT * 4;          // token quads per row (max)
-        constexpr int SB = NQ >= 16 ? 1 : 16 / NQ;  // splits per batch
-        const int nq = Mp / 4;
-        float4 acc[NQ];
+        // Fixed split order => independent of arrival order and of M: each
+        // element is ((0 + p_0) + p_1) + ... over the splits in order.  One
+        // 16-token tile at a time, its 16 loads per split in flight together.
+        const float* src = a.partials + static_cast<size_t>(tile) * a.seg_max * Mp * kTileN + row;
+        const size_t sstride = static_cast<size_t>(Mp) * kTileN;
+#pragma unroll 1
+        for (int j = 0; j < NT; ++j) {
+          if (16 * j >= a.M) break;
+          float acc[16];
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s0 = 0; s0 < u.nseg; s0 += SB) {
-          float4 p[SB][NQ];
+          for (int c = 0; c < 16; ++c) acc[c] = 0.f;
+          for (int sg = 0; sg < u.nseg; ++sg) {
+            float p[16];
 #pragma unroll
-          for (int sb = 0; sb < SB; ++sb)
+            for (int c = 0; c < 16; ++c)
+              p[c] = (16 * j + c < a.M) ? __ldcg(src + sg * sstride + static_cast<size_t>(16 * j + c) * kTileN) : 0.f;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q)
-              if (s0 + sb < u.nseg && q < nq)
-                p[sb][q] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + sb) * sstride + 4 * q));
+            for (int c = 0; c < 16; ++c) acc[c] += p[c];
+          }
 #pragma unroll
-          for (int sb = 0; sb < SB; ++sb)
-#pragma unroll
-            for (int q = 0; q < NQ; ++q)
-              if (s0 + sb < u.nseg && q < nq) {
-                acc[q].x += p[sb][q].x;
-                acc[q].y += p[sb][q].y;
-                acc[q].z += p[sb][q].z;
-                acc[q].w += p[sb][q].w;
-              }
+          for (int c = 0; c < 16; ++c) E[(16 * j + c) * ES + row] = acc[c];
         }
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          if (q < nq) *reinterpret_cast<float4*>(E + row * ES + 4 * q) = acc[q];
         if (et == 0) a.flags[tile] = 0;
       }
       epi_bar();
-      epilogue_tile<NT * 4>(a.e, tile, E, ES, a.M, a.N, et);
+      epilogue_tile<NT * 4, true>(a.e, tile, E, ES, a.M, a.N, et);
       epi_bar();
     }
   }

@@ -33,8 +33,9 @@ struct TcCfg {
   static constexpr int kRing = 144 * 1024;
   static constexpr int kStageBytes = kWBytes + NT * kXBytes;
   static constexpr int kStages = (kRing / kStageBytes) < kMaxStages ? (kRing / kStageBytes) : kMaxStages;
-  static constexpr int kEStride = NT * 16;                 // fp32 per staged row
-  static constexpr int kEBytes = kTileN * kEStride * 4;
+  // staged tile, token-major: E[t * kEStride + row] (+4 pad keeps rows 16-byte aligned)
+  static constexpr int kEStride = kTileN + 4;
+  static constexpr int kEBytes = NT * 16 * kEStride * 4;
   static constexpr int kCols = kAccs * NT * 16;
   static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + kEBytes + 512;
