@@ -310,7 +310,37 @@ def split_leg(args, ws, rank, greedy, temp, ar_agg):
     """N >= 2: ranks (2i, 2i+1) form split pair i -- the target on the even
     GPU, the draft on the odd one, meeting through K6 mailboxes (NVLink peer
     memory).  Each pair decodes its own prompts; tokens are counted once per
-    pair (target ranks), time is the max over all ranks."""
+    pair (target ranks), time is the max over all ranks.
+
+    Guarded: every rank-local failure (including a K6 wait timing out) is
+    caught, all ranks agree on success through one collective, and the leg
+    reports {"error": ...} instead of taking the replica line down with it."""
+    import datetime
+    import torch
+    import torch.distributed as dist
+    import paper_2408_11850_b200 as pk
+    gloo = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=240))
+    err, local = None, None
+    try:
+        local = _split_local(args, ws, rank, greedy, temp, gloo)
+    except Exception as ex:  # noqa: BLE001 -- reported, never fatal
+        err = f"rank {rank}: {type(ex).__name__}: {str(ex)[:200]}"
+    flag = torch.tensor([1.0 if err else 0.0])
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=gloo)
+    if flag.item() > 0:
+        return {"error": err or "a peer rank failed"}
+    one, steps, gammas = local
+    d, e, wl, t = aggregate(one, ws)["pearl"]
+    ar_tps_per_gpu = ar_agg[3] / ar_agg[0] / ws
+    return {"pairs": ws // 2, "placement": "target on even GPU, draft on odd GPU, K6 NVLink mailboxes",
+            "tokens_per_s": round(t / d, 2), "e2e_tokens_per_s": round(t / e, 2),
+            "tokens_per_s_per_pair": round(t / d / (ws // 2), 2),
+            "speedup_vs_single_gpu_ar": round(t / d / (ws // 2) / ar_tps_per_gpu, 3),
+            "mean_accepted_tokens_per_target_fwd": round(pk.mean_tokens_per_target_forward(steps), 3),
+            "alpha_hat": round(pk.empirical_acceptance(steps), 4), "gammas": gammas}
+
+
+def _split_local(args, ws, rank, greedy, temp, gloo):
     import gc
     import torch
     import torch.distributed as dist
@@ -323,11 +353,10 @@ def split_leg(args, ws, rank, greedy, temp, ar_agg):
     tname, dname = llama.PAIRS[args.pair]
     mc = llama.PRESETS[tname if role == split_pair.ROLE_TARGET else dname]
     need = mc.weight_bytes() * 1.1 + (2 << 30)
-    ok = torch.tensor([1.0 if torch.cuda.mem_get_info()[0] > need else 0.0],
-                      device="cpu" if dist.get_backend() == "gloo" else "cuda")
-    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    ok = torch.tensor([1.0 if torch.cuda.mem_get_info()[0] > need else 0.0])
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=gloo)
     if ok.item() < 1:
-        return {"error": "not enough free device memory after the replica leg"}
+        raise RuntimeError("not enough free device memory after the replica leg")
     align = llama.AlignSpec(branch_std=args.branch_std if args.branch_std is not None else PAIR_BRANCH_STD[args.pair],
                             kappa=args.kappa)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -338,8 +367,7 @@ def split_leg(args, ws, rank, greedy, temp, ar_agg):
     gemm = args.gemm_target if is_t else ("tcgen05" if mc.weight_bytes() > 1e9 else "cudacore")
     model = llama.LlamaModel(mc, w, gemm=gemm, max_seq=args.prompt + args.new + 2 * args.gamma_max + 16,
                              max_tokens=64, temperature=1.0 if greedy else temp)
-    gloo = dist.new_group(backend="gloo")
-    remote = split_pair.connect_pair(model, role, peer, gamma_max=args.gamma_max, group=gloo)
+    remote = split_pair.connect_pair(model, role, peer, gamma_max=args.gamma_max, group=gloo, timeout_s=60.0)
     prompts = _prompts(args.warmup + args.steps, args.prompt, mc.vocab, seed=2000 + rank // 2)
 
     def run(i):
@@ -348,31 +376,25 @@ def split_leg(args, ws, rank, greedy, temp, ar_agg):
         return pk.decode_pearl(remote, model, prompts[i], cfg) if is_t else pk.decode_pearl(model, remote, prompts[i],
                                                                                              cfg)
 
-    for i in range(args.warmup):
-        run(i)
-    torch.cuda.synchronize()
-    dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0 = time.perf_counter()
-    ev0.record()
-    res = [run(args.warmup + i) for i in range(args.steps)]
-    ev1.record()
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
+    try:
+        for i in range(args.warmup):
+            run(i)
+        torch.cuda.synchronize()
+        dist.barrier(group=gloo)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        ev0.record()
+        res = [run(args.warmup + i) for i in range(args.steps)]
+        ev1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    finally:
+        remote.link.close()
     toks = sum(len(r.tokens) for r in res) if is_t else 0
     steps = [s for r in res for s in r.steps]
     one = {"pearl": dict(device_s=sum(r.stats["device_s"] for r in res), event_s=ev0.elapsed_time(ev1) / 1e3,
                          wall_s=wall, tokens=toks)}
-    d, e, wl, t = aggregate(one, ws)["pearl"]
-    remote.link.close()
-    ar_tps_per_gpu = ar_agg[3] / ar_agg[0] / ws
-    return {"pairs": ws // 2, "placement": "target on even GPU, draft on odd GPU, K6 NVLink mailboxes",
-            "tokens_per_s": round(t / d, 2), "e2e_tokens_per_s": round(t / e, 2),
-            "tokens_per_s_per_pair": round(t / d / (ws // 2), 2),
-            "speedup_vs_single_gpu_ar": round(t / d / (ws // 2) / ar_tps_per_gpu, 3),
-            "mean_accepted_tokens_per_target_fwd": round(pk.mean_tokens_per_target_forward(steps), 3),
-            "alpha_hat": round(pk.empirical_acceptance(steps), 4),
-            "gammas": sorted(set(g for r in res for g in r.stats.get("gammas", [])))}
+    return one, steps, sorted(set(g for r in res for g in r.stats.get("gammas", [])))
 
 
 def aggregate(results, ws, device=None):
