@@ -114,8 +114,10 @@ PAIR_BRANCH_STD = {"llama2-7b/68m": 5e-4, "dsc-33b/1.3b": 1.7e-4, "llama3-70b/8b
 # target keeps the rest; 0 = shared SMs).  A launch-bound 68M draft on 16 of
 # 148 SMs stops competing with the target's GEMMs for SM slots
 # (tools/green_sweep.sh: 7B/68M PEARL 1011 tok/s shared vs 1153 on 16 SMs;
-# the target forward is HBM-bound and no slower on 132 SMs).  Memory-bound
-# 1.3B / 8B drafts need the whole GPU.
+# the target forward is HBM-bound and no slower on 132 SMs).  tools/green_steps.sh
+# (PEARL step-graph times per gamma) favours 24 SMs at gamma 16 on paper, but the
+# whole decode measures 1179 tok/s on 16 SMs vs 1160 on 24 (target on fewer SMs).
+# Memory-bound 1.3B / 8B drafts need the whole GPU.
 PAIR_DRAFT_SMS = {"llama2-7b/68m": 16, "dsc-33b/1.3b": 0, "llama3-70b/8b": 0, "tiny": 0}
 
 

@@ -23,6 +23,7 @@ reference's tokens and traces.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 from dataclasses import replace
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -387,11 +388,21 @@ class _GammaPlanner:
         old = self.meas.get(k)
         self.meas[k] = seconds if old is None else 0.75 * old + 0.25 * seconds
 
+    def _model_time(self, pre: bool, g: int) -> float:
+        return max(self._t_target(1 if pre else g), g * self.t_d)
+
     def step_time(self, pre: bool, g: int) -> float:
+        """Measured time of the (mode, g) step graph, else the model scaled by
+        the mean measured/model ratio of the steps seen so far (so unexplored
+        draft lengths are priced with the contention already observed)."""
         m = self.meas.get((bool(pre), int(g)))
         if m is not None:
             return m
-        return max(self._t_target(1 if pre else g), g * self.t_d)
+        model = self._model_time(pre, g)
+        if self.meas:
+            logs = [math.log(v / self._model_time(p, q)) for (p, q), v in self.meas.items()]
+            model *= math.exp(sum(logs) / len(logs))
+        return model
 
     def rate(self, alpha: float, g: int) -> float:
         a = min(max(alpha, 1e-6), 1.0 - 1e-9)
