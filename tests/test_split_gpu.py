@@ -116,3 +116,59 @@ def test_split_matches_coresident(split_results):
             continue
         want = _strip(pk.decode_pearl(draft, target, pr, cfg))
         assert got == want, (cfg, got[0], want[0])
+
+
+def test_exchange_wait_times_out_instead_of_hanging():
+    """A K6 wait whose peer never pushes reports PEARL_ERR_TIMEOUT (DeviceError
+    at the Python layer) after its timeout instead of spinning forever."""
+    import ctypes
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2408_11850_b200 import _lib
+    lib = _lib.load()
+    box = ctypes.c_void_p()
+    _lib.check(lib.pearl_mailbox_alloc(int(lib.pearl_mailbox_bytes(0, 8)), ctypes.byref(box)), "alloc")
+    try:
+        ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        dst = torch.zeros(8, dtype=torch.int32, device="cuda")
+        _lib.check(lib.pearl_xfer_wait(box, ctr.data_ptr() + 8, dst.data_ptr(), 8, status.data_ptr(),
+                                       int(0.2e9), torch.cuda.current_stream().cuda_stream), "wait")
+        torch.cuda.synchronize()
+        assert int(status.item()) == _lib.PEARL_ERR_TIMEOUT
+        assert int(ctr[1].item()) == 1  # the receive sequence still advanced (lockstep)
+    finally:
+        lib.pearl_mailbox_free(box)
+
+
+def test_exchange_push_then_wait_same_process():
+    """One push into a (locally mapped) mailbox, then the wait returns the ids."""
+    import ctypes
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2408_11850_b200 import _lib, split_pair
+    lib = _lib.load()
+    V = 64
+    box = ctypes.c_void_p()
+    _lib.check(lib.pearl_mailbox_alloc(int(lib.pearl_mailbox_bytes(3, V)), ctypes.byref(box)), "alloc")
+    try:
+        ctr = torch.zeros(3, dtype=torch.int64, device="cuda")  # send, recv, arrive
+        ids = torch.arange(5, dtype=torch.int32, device="cuda") + 7
+        rows = torch.randn(3, V, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        a = split_pair._XferArgs(box.value, ids.data_ptr(), 5, rows.data_ptr(), 3, V, ctr.data_ptr(), ctr.data_ptr() + 16)
+        _lib.check(lib.pearl_xfer_send(ctypes.byref(a), st), "send")
+        dst = torch.zeros(5, dtype=torch.int32, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(lib.pearl_xfer_wait(box, ctr.data_ptr() + 8, dst.data_ptr(), 5, status.data_ptr(), int(5e9), st),
+                   "wait")
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0 and torch.equal(dst, ids)
+        assert ctr[0].item() == 1 and ctr[1].item() == 1 and ctr[2].item() == 0
+        got = torch.empty(3 * V, dtype=torch.float32)
+        cu = ctypes.CDLL("libcuda.so.1")  # driver API: read the raw mailbox rows back
+        cu.cuMemcpyDtoH_v2.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t]
+        assert cu.cuMemcpyDtoH_v2(got.data_ptr(), box.value + _lib.MAILBOX_ROWS_OFFSET, 3 * V * 4) == 0
+        assert torch.equal(got.view(3, V), rows.cpu())
+    finally:
+        lib.pearl_mailbox_free(box)
