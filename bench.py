@@ -452,7 +452,71 @@ def roofline(target, draft, gamma, args):
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": tr,
             "kernel": f"target window forward ({c.name}, M={M}, ctx={ctx}, {args.gemm_target} GEMMs)",
-            "bytes_per_launch": int(byts), "ms_per_launch": round(t * 1e3, 4), "peak_source": src}
+            "bytes_per_launch": int(byts), "ms_per_launch": round(t * 1e3, 4), "peak_source": src,
+            "gemm_kernel": gemm_roofline(target, M, peak) if args.gemm_target == "tcgen05" else None,
+            "draft_forward": draft_roofline(draft, peak)}
+
+
+def draft_roofline(draft, peak):
+    """K2 chain: one draft token forward (M=1, logits for the pick) as a CUDA
+    graph replayed back to back, CUDA-event timed; bytes = bf16 weights + KV."""
+    import torch
+    toks = torch.full((1,), 5, dtype=torch.int32, device="cuda")
+    pos = torch.tensor([192], dtype=torch.int32, device="cuda")
+    out = torch.empty(1, draft.cfg.vocab, device="cuda")
+    for _ in range(3):
+        draft.forward(toks, 1, pos, 2, out)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        draft.forward(toks, 1, pos, 2, out)
+    n = 50
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(n):
+        g.replay()
+    e.record()
+    e.synchronize()
+    t = s.elapsed_time(e) / 1e3 / n
+    c = draft.cfg
+    byts = c.weight_bytes() + c.kv_bytes_per_token() * 193 + 4 * c.vocab
+    draft.reset_adapter()
+    return {"kernel": f"draft token forward ({c.name}, {draft.gemm}, CUDA graph)", "bytes_per_launch": int(byts),
+            "us_per_launch": round(t * 1e6, 2), "achieved": round(byts / t / 1e9, 1),
+            "frac": round(byts / t / 1e9 / peak, 4)}
+
+
+def gemm_roofline(target, M, peak):
+    """K3 alone (tc_gemm_kernel, ~80-90% of a forward in the ncu launch lists):
+    layer 0's four weight matrices of the target (qkv, o, gate_up, down) at M
+    tokens, launched back to back on one stream, CUDA-event timed; achieved =
+    weight bytes streamed / time."""
+    import torch
+    from paper_2408_11850_b200 import _lib
+    lib = _lib.load()
+    L = target.w["layers"][0]
+    mats = [L["wqkv"], L["wo"], L["w_gate_up"], L["w_down"]]
+    xs = [torch.randn(M, w.shape[1], device="cuda").to(torch.bfloat16) for w in mats]
+    ys = [torch.empty(M, w.shape[0], device="cuda") for w in mats]
+    st = torch.cuda.current_stream().cuda_stream
+
+    def once():
+        for w, x, y in zip(mats, xs, ys):
+            _lib.check(lib.pearl_gemm(1, w.data_ptr(), x.data_ptr(), y.data_ptr(), M, w.shape[0], w.shape[1], 0, st),
+                       "pearl_gemm")
+    for _ in range(3):
+        once()
+    n = 20
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(n):
+        once()
+    e.record()
+    e.synchronize()
+    t = s.elapsed_time(e) / 1e3 / (4 * n)
+    byts = sum(w.numel() * 2 for w in mats) / 4
+    return {"kernel": "tc_gemm_kernel (layer-0 qkv / o / gate_up / down, back to back)", "M": M,
+            "bytes_per_launch": int(byts), "us_per_launch": round(t * 1e6, 2),
+            "achieved": round(byts / t / 1e9, 1), "frac": round(byts / t / 1e9 / peak, 4)}
 
 
 def cpu_baseline(target, draft, prompt, args, greedy, temp):
