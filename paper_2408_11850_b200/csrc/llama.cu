@@ -255,14 +255,12 @@ constexpr int kGemvMaxNormTok = 64;
 // full; the 4 rows an epilogue needs (SwiGLU / RoPE pairs) are then gathered
 // from 4 warps through shared memory.  Per-row arithmetic (chunk order, FMA
 // order, xor tree) is identical for every TOK and RPW (batch invariance).
+// The block-level body: block `bid` of a GEMV grid (also run by the draft's
+// persistent forward, draft_fwd_kernel, one virtual block at a time -- same
+// arithmetic, same bits).  Needs 8 warps; s_rs / s_out are the block's smem.
 template <int TOK, int RPW>
-__global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __restrict__ W, const bf16* __restrict__ X,
-                                                               int M, int N, int K, EpiArgs e, GemvNorm nrm) {
-  __shared__ float s_rs[kGemvMaxNormTok];
-  __shared__ float s_out[RPW == 1 ? kGemvWarps * TOK : 1];
-  pdl_wait();
-  pdl_trigger();
-  if (e.adv_pos != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *e.adv_pos += e.adv_n;
+__device__ __forceinline__ void gemv_block(const bf16* __restrict__ W, const bf16* __restrict__ X, int M, int N, int K,
+                                           const EpiArgs& e, const GemvNorm& nrm, int bid, float* s_rs, float* s_out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (nrm.xh != nullptr) {
     for (int t = warp; t < M; t += kGemvWarps) {
@@ -292,7 +290,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
     }
     __syncthreads();
   }
-  const int n0 = (blockIdx.x * kGemvWarps + warp) * RPW;
+  const int n0 = (bid * kGemvWarps + warp) * RPW;
   const bool active = n0 < N;
   if (RPW > 1 && !active) return;
   const int nchunk = (K + 255) / 256;
@@ -362,7 +360,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
         for (int t = 0; t < TOK; ++t) s_out[warp * TOK + t] = acc[0][t];
       __syncthreads();
       const int grp = threadIdx.x / TOK, t = threadIdx.x % TOK;  // (row quad, token)
-      const int nq = blockIdx.x * kGemvWarps + 4 * grp;
+      const int nq = bid * kGemvWarps + 4 * grp;
       if (grp < kGemvWarps / 4 && t < mt && nq < N) {
         float v[4] = {s_out[(4 * grp) * TOK + t], s_out[(4 * grp + 1) * TOK + t], s_out[(4 * grp + 2) * TOK + t],
                       s_out[(4 * grp + 3) * TOK + t]};
@@ -371,6 +369,17 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
       __syncthreads();
     }
   }
+}
+
+template <int TOK, int RPW>
+__global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __restrict__ W, const bf16* __restrict__ X,
+                                                               int M, int N, int K, EpiArgs e, GemvNorm nrm) {
+  __shared__ float s_rs[kGemvMaxNormTok];
+  __shared__ float s_out[RPW == 1 ? kGemvWarps * TOK : 1];
+  pdl_wait();
+  pdl_trigger();
+  if (e.adv_pos != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *e.adv_pos += e.adv_n;
+  gemv_block<TOK, RPW>(W, X, M, N, K, e, nrm, blockIdx.x, s_rs, s_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -404,14 +413,15 @@ struct AttnArgs {
   long long slot_stride;
 };
 
+// Block-level body for head h, token group tg; run by warps 0..3 of the
+// block (named barrier 2 over those 128 threads), also from the draft's
+// persistent forward.
+__device__ __forceinline__ void attn_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+
 template <int HD>
-__global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs a) {
+__device__ __forceinline__ void attention_block(AttnArgs a, int h, int tg, unsigned char* attn_smem) {
   constexpr int PER = HD / 32;  // dims per lane (2 or 4)
-  extern __shared__ __align__(16) unsigned char attn_smem[];
-  pdl_wait();
-  pdl_trigger();
-  const int h = blockIdx.x;
-  const int t0 = blockIdx.y * a.tpb;                  // first window token of this block
+  const int t0 = tg * a.tpb;                          // first window token of this block
   const int MT = min(a.tpb, a.M - t0);                // tokens handled here
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p0 = a.tok_pos ? a.tok_pos[t0] : *a.pos + a.pos_add + t0;  // position of the block's first token
@@ -429,13 +439,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs 
   float* st = st_all + static_cast<size_t>(warp) * MT * (HD + 2);
   bf16* Qs = reinterpret_cast<bf16*>(st_all + static_cast<size_t>(kAttnWarps) * a.tpb * (HD + 2));  // [MT][HD]
   bf16* Vw = Qs + a.tpb * HD + static_cast<size_t>(warp) * kAttnLanesPos * HD;  // this warp's V chunk
-  for (int i = threadIdx.x; i < MT * HD / 8; i += blockDim.x) {
+  for (int i = threadIdx.x; i < MT * HD / 8; i += kAttnWarps * 32) {
     const int t = i / (HD / 8), v = i % (HD / 8);
     reinterpret_cast<uint4*>(Qs + t * HD)[v] =
         *reinterpret_cast<const uint4*>(a.q + (static_cast<size_t>(t0 + t) * a.H + h) * HD + v * 8);
   }
   for (int i = lane; i < MT * (HD + 2); i += 32) st[i] = (i % (HD + 2) == HD) ? -INFINITY : 0.f;
-  __syncthreads();
+  attn_bar();
   for (int c = warp; c < n_chunks; c += kAttnWarps) {
     const int j = c * kAttnLanesPos + lane;  // this lane's position
     const bool have = j < ctx_max;
@@ -519,9 +529,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs 
     }
     __syncwarp();  // Vw is overwritten by the warp's next chunk
   }
-  __syncthreads();
+  attn_bar();
   // merge the warps' states in warp order
-  for (int i = threadIdx.x; i < MT * HD; i += blockDim.x) {
+  for (int i = threadIdx.x; i < MT * HD; i += kAttnWarps * 32) {
     const int t = i / HD, d = i % HD;
     float mx = -INFINITY;
 #pragma unroll
@@ -538,6 +548,14 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs 
     }
     a.o[(static_cast<size_t>(t0 + t) * a.H + h) * HD + d] = __float2bfloat16(O / L);
   }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnWarps * 32, 2) attention_kernel(AttnArgs a) {
+  extern __shared__ __align__(16) unsigned char attn_smem[];
+  pdl_wait();
+  pdl_trigger();
+  attention_block<HD>(a, blockIdx.x, blockIdx.y, attn_smem);
 }
 
 size_t attention_smem_bytes(int tpb, int hd) {
