@@ -104,6 +104,8 @@ class BatchRuntime:
         self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         self.draft_stream = torch.cuda.Stream(device=dev)
         self.target_stream = torch.cuda.Stream(device=dev)
+        self.graphs = {}
+        self.tcap = B * (g + 2)  # target window tokens per step (max)
 
     # -- helpers ----------------------------------------------------------------
     def load_table(self, s: int, i: int, rng: RandomStream) -> None:
@@ -114,21 +116,27 @@ class BatchRuntime:
         (the previous step's copies completed at its read-back sync)."""
         self._off = 0
 
-    def upload(self, chunks: List[np.ndarray]) -> List[torch.Tensor]:
+    def upload(self, chunks: List[np.ndarray], caps: Optional[List[int]] = None) -> List[torch.Tensor]:
         """Copy int arrays to the device in one transfer on the current stream;
-        returns device views (int32 arrays become int32 views of the int64 slab)."""
+        returns device views (int32 arrays become int32 views of the int64 slab).
+        With `caps`, chunk i occupies cap[i] elements whatever its length, so a
+        fixed sequence of capped uploads at the start of a step lands at fixed
+        device addresses (the inputs of the captured step graphs)."""
         host = self.ibuf_host.numpy()
         views, off = [], getattr(self, "_off", 0)
         start = off
-        for a in chunks:
+        for ci, a in enumerate(chunks):
             n = len(a)
+            cap = max(n, caps[ci]) if caps is not None else n
+            if caps is not None and n > caps[ci]:
+                raise ValueError("batched upload exceeds its capped region")
             if a.dtype == np.int64:
                 host[off:off + n] = a
                 views.append(("i64", off, n))
-                off += n
+                off += cap
             else:
-                m = (n + 1) // 2
-                host[off:off + m].view(np.int32)[:n] = a.astype(np.int32)
+                m = (cap + 1) // 2
+                host[off:off + (n + 1) // 2].view(np.int32)[:n] = a.astype(np.int32)
                 views.append(("i32", off, n))
                 off += m
         if off > len(host):
@@ -165,6 +173,17 @@ class BatchRuntime:
             _device.ptr(self.tables[1, i]), U_TABLE, _addr(self.cursors[1], i), invt, flags,
             _device.ptr(self.verdict[i]), None, _device.ptr(self.work[i]), _device.stream_ptr(stream)),
             "spec_verify (batched)")
+
+    def replay(self, key: tuple, fn, stream) -> None:
+        """Run fn(stream) as a CUDA graph keyed by its shape (captured on first use)."""
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn(torch.cuda.current_stream())
+            self.graphs[key] = g
+        with torch.cuda.stream(stream):
+            g.replay()
 
     def row(self, t: torch.Tensor, r: int) -> int:
         return int(t.data_ptr()) + r * self.V * 4
@@ -267,24 +286,29 @@ def _draft_prepare(rt: BatchRuntime, act: List[_Seq], gamma: int, par: int):
     posj = [np.array([s.dpos + m0s[r] + j - 1 for r, s in enumerate(act)], np.int32) for j in range(1, gamma)]
     rows0 = np.array([rt.row(rt.stage, r) for r in last], np.int64)
     rowsj = [np.array([rt.row(rt.qbuf[par, j], r) for r in range(n)], np.int64) for j in range(1, gamma)]
+    B, c0 = rt.B, rt.tcap
     bufs = rt.upload([np.array(toks, np.int32), np.array(slots, np.int32), np.array(pos, np.int32), slot_arr,
-                      rows0, rt.stream_ptrs(0, act)] + posj + rowsj)
-    return (bufs, len(toks)), [rt.row(rt.stage, r) for r in last], m0s
+                      rows0, rt.stream_ptrs(0, act)] + posj + rowsj,
+                     caps=[c0, c0, c0, B, B, 2 * B] + [B] * (gamma - 1) + [B] * (gamma - 1))
+    return (bufs, len(toks), par), [rt.row(rt.stage, r) for r in last], m0s
 
 
 def _draft_launch(rt: BatchRuntime, prep, n: int, gamma: int, par: int, invt: float, greedy: bool, stream) -> None:
-    """gamma draft iterations for every active sequence on `stream`: x_j lands in rt.xs[j, rank]."""
-    (bufs, n_tok) = prep
+    """gamma draft iterations for every active sequence on `stream` (one CUDA
+    graph per (catch-up tokens, sequences, gamma, parity)): x_j lands in rt.xs[j, rank]."""
+    (bufs, n_tok, par) = prep
     t0, s0, p0, sl, r0, sp = bufs[:6]
     pj = bufs[6:6 + gamma - 1]
     rj = bufs[6 + gamma - 1:]
     d = rt.draft
-    with torch.cuda.stream(stream):
-        d.forward_slots(t0, n_tok, s0, p0, rt.stage, stream)
-        rt.pick(r0, n, _addr(rt.xs[0]), sp, invt, greedy, stream)
+
+    def body(st):
+        d.forward_slots(t0, n_tok, s0, p0, rt.stage, st)
+        rt.pick(r0, n, _addr(rt.xs[0]), sp, invt, greedy, st)
         for j in range(1, gamma):
-            d.forward_slots(rt.xs[j - 1], n, sl, pj[j - 1], rt.qbuf[par, j], stream)
-            rt.pick(rj[j - 1], n, _addr(rt.xs[j]), sp, invt, greedy, stream)
+            d.forward_slots(rt.xs[j - 1], n, sl, pj[j - 1], rt.qbuf[par, j], st)
+            rt.pick(rj[j - 1], n, _addr(rt.xs[j]), sp, invt, greedy, st)
+    rt.replay(("draft", n_tok, n, gamma, par, invt, greedy), body, stream)
 
 
 def _read_back(rt: BatchRuntime, n: int, gamma: int) -> tuple:
@@ -302,12 +326,27 @@ def _read_back(rt: BatchRuntime, n: int, gamma: int) -> tuple:
     return verdict, xs, cur
 
 
+def _single(kind: str, draft, target, prompts, cfg, seeds):
+    """B == 1: the graph-captured single-sequence engine (same tokens and
+    traces by construction; it is the faster implementation of a batch of one)."""
+    from . import fastpath
+    seed = int(seeds[0]) if seeds is not None else derive_seed(cfg.seed, 0)
+    c = replace(cfg, seed=seed)
+    if kind == "pearl":
+        return [fastpath.decode_pearl(draft, target, prompts[0], c)]
+    if kind == "sd":
+        return [fastpath.decode_sd(draft, target, prompts[0], c)]
+    return [fastpath.decode_autoregressive(target, prompts[0], c)]
+
+
 def decode_pearl_batch(draft: LlamaModel, target: LlamaModel, prompts: Sequence[Sequence[int]], cfg,
                        seeds: Optional[Sequence[int]] = None) -> list:
     """decode_pearl (engines.py:532-591) for B prompts in lockstep; result i
     equals decode_pearl(draft, target, prompts[i], replace(cfg, seed=seeds[i]))
     (seeds default to the CLI's derive_seed(cfg.seed, i))."""
     from .engines import DecodeResult, StepTrace, finalize_step
+    if len(prompts) == 1:
+        return _single("pearl", draft, target, prompts, cfg, seeds)
     gamma = cfg.gamma
     rt, seqs, rngs, stats = _setup(target, draft, prompts, cfg, seeds, "pearl")
     invt, greedy = inv_temp(cfg.temperature), bool(cfg.greedy)
@@ -333,7 +372,8 @@ def decode_pearl_batch(draft: LlamaModel, target: LlamaModel, prompts: Sequence[
             ttok += w
             tslot += [s.slot] * len(w)
             tpos += list(range(len(s.committed) - 1, len(s.committed) - 1 + len(w)))
-        tt, ts, tp = rt.upload([np.array(ttok, np.int32), np.array(tslot, np.int32), np.array(tpos, np.int32)])
+        tt, ts, tp = rt.upload([np.array(ttok, np.int32), np.array(tslot, np.int32), np.array(tpos, np.int32)],
+                               caps=[rt.tcap] * 3)
         prep, q0, m0s = _draft_prepare(rt, act, gamma, par)
         ptr_rows = []
         for r, s in enumerate(act):
@@ -344,8 +384,8 @@ def decode_pearl_batch(draft: LlamaModel, target: LlamaModel, prompts: Sequence[
         ptrs, pend = flat[0], flat[1:]
         rt.draft_stream.wait_stream(main)
         rt.target_stream.wait_stream(main)
-        with torch.cuda.stream(rt.target_stream):
-            target.forward_slots(tt, len(ttok), ts, tp, rt.trows, rt.target_stream)
+        nt = len(ttok)
+        rt.replay(("target", nt), lambda st: target.forward_slots(tt, nt, ts, tp, rt.trows, st), rt.target_stream)
         _draft_launch(rt, prep, n, gamma, par, invt, greedy, rt.draft_stream)
         main.wait_stream(rt.draft_stream)
         main.wait_stream(rt.target_stream)
@@ -404,6 +444,8 @@ def decode_sd_batch(draft: LlamaModel, target: LlamaModel, prompts: Sequence[Seq
                     seeds: Optional[Sequence[int]] = None) -> list:
     """decode_sd (engines.py:344-394) for B prompts in lockstep."""
     from .engines import DecodeResult, StepTrace
+    if len(prompts) == 1:
+        return _single("sd", draft, target, prompts, cfg, seeds)
     gamma = cfg.gamma
     rt, seqs, rngs, stats = _setup(target, draft, prompts, cfg, seeds, "sd")
     invt, greedy = inv_temp(cfg.temperature), bool(cfg.greedy)
@@ -420,6 +462,9 @@ def decode_sd_batch(draft: LlamaModel, target: LlamaModel, prompts: Sequence[Seq
         main = torch.cuda.current_stream()
         rt.ev[0].record()
         rt.begin_step()
+        # same staging layout as a PEARL step (target region first), so the
+        # draft block's captured graph reads the same fixed addresses
+        rt.upload([np.zeros(0, np.int32)] * 3, caps=[rt.tcap] * 3)
         prep, q0, m0s = _draft_prepare(rt, act, gamma, 0)
         # target window [committed[-1]] + xs: the ids come from the device picks
         tslot, tpos, offs, first = [], [], [], []
@@ -479,6 +524,8 @@ def decode_autoregressive_batch(target: LlamaModel, prompts: Sequence[Sequence[i
     `block` steps of (one slot-mode forward over the B last tokens -> B picks)
     per host sync."""
     from .engines import DecodeResult, StepTrace
+    if len(prompts) == 1:
+        return _single("ar", None, target, prompts, cfg, seeds)
     rt, seqs, rngs, stats = _setup(target, None, prompts, cfg, seeds, "ar")
     invt, greedy = inv_temp(cfg.temperature), bool(cfg.greedy)
     t_t = target.latency.forward_time
