@@ -200,6 +200,7 @@ def run_gpu(args):
     agg = aggregate(results, ws)
     # roofline of the dominant kernel sequence: one target window forward
     rl = roofline(target, draft, args.gamma, args)
+    split_model = split_pair_model(target, draft, results["pearl"]["alpha"]) if ws == 1 else None
     target_bytes, draft_bytes = target.cfg.weight_bytes(), draft.cfg.weight_bytes()
     sweep = batch_sweep(target, draft, args, sweep_bs, greedy, temp, ws) if sweep_bs else None
     cpu = None
@@ -265,6 +266,7 @@ def run_gpu(args):
         "exact_cdf_fallbacks": int(results["pearl"]["fallbacks"]),
         "roofline": rl,
         "split_pair": split,
+        "split_pair_model": split_model,
         "batch_sweep": sweep,
         "cpu_baseline": cpu,
         "clocks": clocks,
@@ -274,6 +276,37 @@ def run_gpu(args):
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def split_pair_model(target, draft, alpha):
+    """PREDICTED (not measured) tokens/s of one split pair -- draft on its own
+    GPU, target on another -- from this run's own measurements:
+    target window forward times t_t(M) and draft token time t_d (forward + pick)
+    each timed alone on this B200, and this run's PEARL alpha-hat, through the
+    stationary PEARL rate E(alpha, g) / max(t_t(g) + t_v, g t_d + t_x)
+    (fastpath.pearl_tokens_per_step; t_v = K1 + commit, t_x = K6 exchange).
+    Reported because this sandbox has one GPU; the split path itself is
+    parity-tested (tests/test_split_gpu.py)."""
+    if alpha is None:
+        return None
+    from paper_2408_11850_b200.fastpath import pearl_tokens_per_step
+    t_t = {m: target.measure_forward_time(m) for m in (1, 4, 8, 16, 32)}
+    t_d = draft.measure_forward_time(1) + 15e-6
+    target.reset_adapter()
+    draft.reset_adapter()
+    t_v, t_x = 60e-6, 10e-6
+    ks = sorted(t_t)
+
+    def tt(m):
+        for lo, hi in zip(ks, ks[1:]):
+            if m <= hi:
+                return t_t[lo] + (t_t[hi] - t_t[lo]) * (m - lo) / (hi - lo)
+        return t_t[ks[-1]] * m / ks[-1]
+    best = max(((pearl_tokens_per_step(alpha, g) / max(tt(g) + t_v, g * t_d + t_x), g)
+                for g in (1, 2, 3, 4, 6, 8, 12, 16, 20, 24, 32)))
+    return {"kind": "model, not a measurement (1-GPU sandbox)", "predicted_tokens_per_s": round(best[0], 1),
+            "gamma": best[1], "alpha_hat": round(alpha, 4), "t_draft_ms": round(t_d * 1e3, 4),
+            "t_target_ms": {str(m): round(v * 1e3, 4) for m, v in t_t.items()}}
 
 
 def batch_sweep(target, draft, args, bs, greedy, temp, ws):
