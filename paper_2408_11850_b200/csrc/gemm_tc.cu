@@ -50,7 +50,6 @@ struct TcArgs {
   // weight row run), so HBM keeps streaming through this kernel's tail
   const __nv_bfloat16* nW;
   int nN, nK, nG, next_pf;
-  int w_evict_first;  // W tiles loaded with an L2 evict-first hint (streamed once per forward)
 };
 
 // ---- kernel ------------------------------------------------------------------
@@ -109,17 +108,12 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
       // ---- TMA producer: iterations r0..r1 in order (tile = x / KB, kb = x % KB)
       const uint32_t bytes = stage_bytes;
       const int npre = min(stages, total);
-      const uint64_t pol = l2_evict_first();
       // W does not depend on the previous kernel: request it before the PDL wait
       for (int it = 0; it < npre; ++it) {
         const long long x = r0 + it;
         unsigned char* st = smem + it * stage_bytes;
         mbar_expect_tx(&full[it], bytes);
-        if (a.w_evict_first)
-          tma_load_2d_hint(st, &tmW, &full[it], static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN,
-                           pol);
-        else
-          tma_load_2d(st, &tmW, &full[it], static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN);
+        tma_load_2d(st, &tmW, &full[it], static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN);
       }
       // and the next tiles into L2: HBM keeps streaming this GEMM's weights
       // while the predecessor (attention / RMSNorm / GEMM tail) finishes
@@ -143,10 +137,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         unsigned char* st = smem + s * stage_bytes;
         const int kc = static_cast<int>(x % a.KB) * kTileK;
         mbar_expect_tx(&full[s], bytes);
-        if (a.w_evict_first)
-          tma_load_2d_hint(st, &tmW, &full[s], kc, static_cast<int>(x / a.KB) * kTileN, pol);
-        else
-          tma_load_2d(st, &tmW, &full[s], kc, static_cast<int>(x / a.KB) * kTileN);
+        tma_load_2d(st, &tmW, &full[s], kc, static_cast<int>(x / a.KB) * kTileN);
         for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
       }
     }
@@ -398,8 +389,6 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   {
     const char* v = std::getenv("PEARL_L2PF");
     ctx.l2_prefetch_iters = v ? std::max(0, std::atoi(v)) : kDefaultL2Prefetch;
-    const char* ef = std::getenv("PEARL_W_EVICT_FIRST");
-    ctx.w_evict_first = ef ? std::atoi(ef) : 1;
     const char* w = std::getenv("PEARL_NEXTPF");
     ctx.next_prefetch_iters = w ? std::max(0, std::atoi(w)) : kDefaultNextPrefetch;
   }
@@ -475,7 +464,6 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
                                                                       ((next.K + kTileK - 1) / kTileK)))
                 : 0;
   a.next_pf = ctx.next_prefetch_iters;
-  a.w_evict_first = ctx.w_evict_first;
   if (static_cast<size_t>(tiles) * a.seg_max * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
       tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");

@@ -34,8 +34,7 @@ struct TcGemmCtx {
   int max_tokens = 0;
   int num_sms = 148;
   int min_plan_splits = 1;
-  int next_prefetch_iters = 0;
-  int w_evict_first = 1;  // streamed weights marked L2 evict-first (PEARL_W_EVICT_FIRST=0 disables)  // k-blocks of the NEXT GEMM per CTA prefetched into L2 in the tail
+  int next_prefetch_iters = 0;  // k-blocks of the NEXT GEMM per CTA prefetched into L2 in the tail
   int l2_prefetch_iters = 0;  // next-GEMM weight tiles per CTA requested into L2 (0: off)  // workspace sized for at least this many splits (microbenchmarks)
   // per weight matrix, keyed by (address, N, K): a map encodes the shape too
   std::map<std::tuple<const void*, int, int>, TcWeightMap> wmaps;
