@@ -43,13 +43,6 @@ struct TcArgs {
   EpiArgs e;
   float* partials;
   int* flags;
-  int l2_prefetch;  // W tiles past the ring requested into L2 before the PDL wait
-  // the NEXT GEMM of the forward (weights [nN, nK]): once this CTA's producer
-  // has issued its last load, warp 0 requests the first next_pf k-blocks the
-  // same CTA index will stream there into L2 (plain bulk prefetches, one per
-  // weight row run), so HBM keeps streaming through this kernel's tail
-  const __nv_bfloat16* nW;
-  int nN, nK, nG, next_pf;
 };
 
 // ---- kernel ------------------------------------------------------------------
@@ -115,13 +108,6 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         mbar_expect_tx(&full[it], bytes);
         tma_load_2d(st, &tmW, &full[it], static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN);
       }
-      // and the next tiles into L2: HBM keeps streaming this GEMM's weights
-      // while the predecessor (attention / RMSNorm / GEMM tail) finishes
-      const int npf = min(total, npre + a.l2_prefetch);
-      for (int it = npre; it < npf; ++it) {
-        const long long x = r0 + it;
-        tma_prefetch_l2_2d(&tmW, static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN);
-      }
       asm volatile("griddepcontrol.wait;" ::: "memory");
       if (blockIdx.x == 0 && a.e.adv_pos != nullptr) *a.e.adv_pos += a.e.adv_n;
       for (int it = 0; it < npre; ++it) {
@@ -139,30 +125,6 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         mbar_expect_tx(&full[s], bytes);
         tma_load_2d(st, &tmW, &full[s], kc, static_cast<int>(x / a.KB) * kTileN);
         for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
-      }
-    }
-    __syncwarp();
-    if (a.next_pf > 0 && a.nW != nullptr) {
-      const int nKB = (a.nK + kTileK - 1) / kTileK;
-      const long long nT = static_cast<long long>((a.nN + kTileN - 1) / kTileN) * nKB;
-      if (blockIdx.x < a.nG) {
-        const long long q0 = static_cast<long long>(blockIdx.x) * nT / a.nG;
-        const long long q1 = min(static_cast<long long>(blockIdx.x + 1) * nT / a.nG, q0 + a.next_pf);
-        // runs of consecutive k-blocks inside one tile: rows x contiguous bytes
-        for (long long x = q0; x < q1;) {
-          const int tile = static_cast<int>(x / nKB), kb = static_cast<int>(x % nKB);
-          const int len = static_cast<int>(min(q1 - x, static_cast<long long>(nKB - kb)));
-          const int kc = kb * kTileK, kn = min(len * kTileK, a.nK - kc);
-          const uint32_t bytes = static_cast<uint32_t>(kn) * 2u;
-          for (int r = lane; r < kTileN; r += 32) {
-            const int row = tile * kTileN + r;
-            if (row < a.nN && (bytes & 15u) == 0)
-              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.nW + static_cast<size_t>(row) * a.nK + kc),
-                           "r"(bytes)
-                           : "memory");
-          }
-          x += len;
-        }
       }
     }
   } else if (warp == 1) {
@@ -270,12 +232,6 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
 }
 
 // ---- host side ---------------------------------------------------------------
-// W tiles per CTA requested into L2 ahead of the ring before the PDL wait
-// (PEARL_L2PF overrides).
-constexpr int kDefaultL2Prefetch = 0;
-// k-blocks of the next GEMM per CTA requested into L2 in this GEMM's tail
-// (PEARL_NEXTPF overrides).
-constexpr int kDefaultNextPrefetch = 0;
 
 namespace {
 
@@ -386,12 +342,6 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   });
   PEARL_CUDA_TRY(g_attr_err);
   ctx.max_tokens = c.max_tokens;
-  {
-    const char* v = std::getenv("PEARL_L2PF");
-    ctx.l2_prefetch_iters = v ? std::max(0, std::atoi(v)) : kDefaultL2Prefetch;
-    const char* w = std::getenv("PEARL_NEXTPF");
-    ctx.next_prefetch_iters = w ? std::max(0, std::atoi(w)) : kDefaultNextPrefetch;
-  }
   const int hd = c.head_dim;
   const int shapes[5][2] = {{(c.n_heads + 2 * c.n_kv_heads) * hd, c.d_model},
                             {c.d_model, c.n_heads * hd},
@@ -456,14 +406,7 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.e = e;
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;
-  a.l2_prefetch = ctx.l2_prefetch_iters;
-  a.nW = next.W;
-  a.nN = next.N;
-  a.nK = next.K;
-  a.nG = next.W ? static_cast<int>(std::min<long long>(ctx.num_sms, static_cast<long long>((next.N + kTileN - 1) / kTileN) *
-                                                                      ((next.K + kTileK - 1) / kTileK)))
-                : 0;
-  a.next_pf = ctx.next_prefetch_iters;
+  (void)next;  // (L2 prefetch of the next GEMM's weights: measured slower, profiles/README.md)
   if (static_cast<size_t>(tiles) * a.seg_max * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
       tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");

@@ -33,9 +33,7 @@ struct TcGemmCtx {
   int n_flags = 0;
   int max_tokens = 0;
   int num_sms = 148;
-  int min_plan_splits = 1;
-  int next_prefetch_iters = 0;  // k-blocks of the NEXT GEMM per CTA prefetched into L2 in the tail
-  int l2_prefetch_iters = 0;  // next-GEMM weight tiles per CTA requested into L2 (0: off)  // workspace sized for at least this many splits (microbenchmarks)
+  int min_plan_splits = 1;  // workspace sized for at least this many splits (microbenchmarks)
   // per weight matrix, keyed by (address, N, K): a map encodes the shape too
   std::map<std::tuple<const void*, int, int>, TcWeightMap> wmaps;
 };

@@ -82,14 +82,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// Request a tile into L2 only (no smem, no barrier): used before the PDL wait
-// to keep HBM streaming while the previous kernel drains.
-__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
-
 __device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem_tile) {
   // K-major SWIZZLE_128B canonical layout: rows of 128 B, 8-row groups 1024 B
   // apart (SBO = 1024 B), LBO = 16 B (unused for swizzled K-major), version 1.
