@@ -98,33 +98,37 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---- TMA producer: iterations r0..r1 in order (tile = x / KB, kb = x % KB)
+      // ---- TMA producer: iterations r0..r1 in order (tile = x / KB, kb = x % KB),
+      // walked with incremental (tile, kb) counters: no 64-bit divisions in the
+      // issue loop (this single thread's loop is on the streaming critical path)
       const uint32_t bytes = stage_bytes;
       const int npre = min(stages, total);
+      const int kb_start = static_cast<int>(r0 % a.KB), tile_start = static_cast<int>(r0 / a.KB);
+      int kb = kb_start, tile = tile_start;
       // W does not depend on the previous kernel: request it before the PDL wait
       for (int it = 0; it < npre; ++it) {
-        const long long x = r0 + it;
         unsigned char* st = smem + it * stage_bytes;
         mbar_expect_tx(&full[it], bytes);
-        tma_load_2d(st, &tmW, &full[it], static_cast<int>(x % a.KB) * kTileK, static_cast<int>(x / a.KB) * kTileN);
+        tma_load_2d(st, &tmW, &full[it], kb * kTileK, tile * kTileN);
+        if (++kb == a.KB) { kb = 0; ++tile; }
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
       if (blockIdx.x == 0 && a.e.adv_pos != nullptr) *a.e.adv_pos += a.e.adv_n;
+      int kx = kb_start;
       for (int it = 0; it < npre; ++it) {
-        const long long x = r0 + it;
         unsigned char* st = smem + it * stage_bytes;
-        for (int j = 0; j < NT; ++j)
-          tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[it], static_cast<int>(x % a.KB) * kTileK, j * kTokTile);
+        for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[it], kx * kTileK, j * kTokTile);
+        if (++kx == a.KB) kx = 0;
       }
       for (int it = npre; it < total; ++it) {
-        const long long x = r0 + it;
         const int s = it % stages;
         mbar_wait(&empty[s], ((it / stages) - 1) & 1);
         unsigned char* st = smem + s * stage_bytes;
-        const int kc = static_cast<int>(x % a.KB) * kTileK;
+        const int kc = kb * kTileK;
         mbar_expect_tx(&full[s], bytes);
-        tma_load_2d(st, &tmW, &full[s], kc, static_cast<int>(x / a.KB) * kTileN);
+        tma_load_2d(st, &tmW, &full[s], kc, tile * kTileN);
         for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
+        if (++kb == a.KB) { kb = 0; ++tile; }
       }
     }
   } else if (warp == 1) {
