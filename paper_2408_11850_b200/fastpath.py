@@ -363,7 +363,11 @@ class _GammaPlanner:
         self.t_d, self.t_t = cal
         self.meas = target.__dict__.setdefault("_pearl_steptimes_" + str(id(draft)), {})
         self.gmax = gamma_max
-        self.acc, self.exam = 3.0, 4.0  # prior alpha 0.75
+        # prior: 8 pseudo-observations at the pair's acceptance so far (0.75
+        # before any decode), so a decode does not re-learn alpha from scratch
+        self.pair = target.__dict__.setdefault("_pearl_alpha_" + str(id(draft)), [3.0, 4.0])
+        a0 = self.pair[0] / self.pair[1]
+        self.acc, self.exam = 8.0 * a0, 8.0
         self.gamma = gamma0
         self.started = False
 
@@ -380,6 +384,9 @@ class _GammaPlanner:
     def observe(self, accepted: int, rejected: int) -> None:
         self.acc += accepted
         self.exam += accepted + rejected
+        if hasattr(self, "pair"):
+            self.pair[0] += accepted
+            self.pair[1] += accepted + rejected
 
     def observe_time(self, pre: bool, g: int, seconds: float) -> None:
         """Measured device time of one step graph (co-resident path only: the
@@ -450,19 +457,19 @@ def choose_gamma(cfg, target: LlamaModel, draft: LlamaModel) -> int:
 def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], cfg, concurrent: bool = True):
     from .engines import DecodeResult, StepTrace, finalize_step
     planner = _GammaPlanner(target, draft, cfg.gamma_max, cfg.gamma) if cfg.adaptive_gamma else None
-    gamma = planner.next_gamma() if planner else cfg.gamma
-    gmax = max(cfg.gamma_max, gamma, cfg.gamma)
+    gmax = max(cfg.gamma_max, cfg.gamma)
     t_d1 = draft.latency.forward_time  # (measured before the caches are filled)
     t_t = target.latency.forward_time
     rt = _runtime(target, draft, gmax)
     seq0 = _seq0(target, prefix)
     n0 = len(seq0)
+    invt = inv_temp(cfg.temperature)
+    gamma = planner.next_gamma() if planner else cfg.gamma
     stats = _new_stats(gamma=gamma, gammas=[])
     rt.reset(seq0, stats)
     root = RandomStream(cfg.seed)
     tab_d = _Tables(rt, rt.u_draft, None if cfg.greedy else root.split(0), S_DCUR)
     tab_v = _Tables(rt, rt.u_verify, None if cfg.greedy else root.split(1), S_VCUR)
-    invt = inv_temp(cfg.temperature)
     _precapture_pearl(rt, planner, gamma, invt, bool(cfg.greedy), bool(concurrent))
     committed: List[int] = list(seq0)
     pending: List[int] = []
