@@ -111,14 +111,14 @@ def _prompts(n, P, V, seed):
 # alignment knob per pair, calibrated on B200 to alpha-hat ~0.9 at T=1 (tools/calib_alpha.py)
 PAIR_BRANCH_STD = {"llama2-7b/68m": 5e-4, "dsc-33b/1.3b": 1.7e-4, "llama3-70b/8b": 8e-5, "tiny": 2e-4}
 # SMs of the green-context partition PEARL's concurrent draft runs on (the
-# target keeps the rest; 0 = shared SMs).  A launch-bound 68M draft on 16 of
-# 148 SMs stops competing with the target's GEMMs for SM slots
-# (tools/green_sweep.sh: 7B/68M PEARL 1011 tok/s shared vs 1153 on 16 SMs;
-# the target forward is HBM-bound and no slower on 132 SMs).  tools/green_steps.sh
-# (PEARL step-graph times per gamma) favours 24 SMs at gamma 16 on paper, but the
-# whole decode measures 1179 tok/s on 16 SMs vs 1160 on 24 (target on fewer SMs).
+# target keeps the rest; 0 = shared SMs; the driver rounds to 8-SM groups).  On
+# its own SMs the 68M draft stops competing with the target's GEMM CTAs for SM
+# slots, and enough of them let it keep up with long draft blocks
+# (tools/green_sweep.sh, current kernels, T=1: PEARL 1165 tok/s at 16-24 SMs,
+# 1285-1295 at 32, 1287-1365 at 40 with gamma 16-32, 1165-1288 at 48; the
+# target's stream-K grid shrinks with it -- AR 307 -> 298 tok/s at 40).
 # Memory-bound 1.3B / 8B drafts need the whole GPU.
-PAIR_DRAFT_SMS = {"llama2-7b/68m": 16, "dsc-33b/1.3b": 0, "llama3-70b/8b": 0, "tiny": 0}
+PAIR_DRAFT_SMS = {"llama2-7b/68m": 40, "dsc-33b/1.3b": 0, "llama3-70b/8b": 0, "tiny": 0}
 
 
 def run_gpu(args):
