@@ -394,6 +394,12 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
         draft_sms = int(os.environ.get("PEARL_DRAFT_SMS", "0"))
     green = None
     target_sms = 0
+    if draft_sms > 0 and PRESETS[PAIRS[pair][0]].vocab > 65536:
+        # the pick / K1 kernels run 16-CTA clusters at V > 65536, which a
+        # partition's GPC slices cannot host (cudaErrorInvalidClusterSize)
+        import warnings
+        warnings.warn("green-context draft partition needs V <= 65536 (8-CTA clusters); using shared SMs")
+        draft_sms = 0
     if draft_sms > 0:
         _device.require_cuda()
         ds, ts = ctypes.c_void_p(), ctypes.c_void_p()
@@ -415,8 +421,10 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
         gemm_draft = "tcgen05" if dc.weight_bytes() > 1e9 else "cudacore"
     # the CUDA-core engine's fused-norm prologue takes <= 64 tokens per pass
     draft_tokens = max_tokens if gemm_draft == "tcgen05" else min(max_tokens, 64)
+    # a tcgen05 draft on its own partition sizes its persistent grids to it
     draft = LlamaModel(dc, dw, gemm=gemm_draft, max_seq=max_seq, max_tokens=draft_tokens, temperature=temperature,
-                       l2_resident=l2_draft, n_slots=n_slots)
+                       l2_resident=l2_draft, n_slots=n_slots,
+                       sm_count=green[2] if green is not None and gemm_draft == "tcgen05" else 0)
     if green is not None:
         target.green_partition = green  # (draft stream, target stream, draft SMs, target SMs)
     return target, draft
