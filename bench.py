@@ -169,6 +169,7 @@ def run_gpu(args):
         return pk.decode_autoregressive(target, prompts[i], cfg_for(1, 17 + i))
 
     results = {}
+    timed_results = {}
     clocks = None
     for kind in ("ar", "sd", "sd8", "sd16", "pearl"):  # PEARL last: its clocks are sampled
         for i in range(args.warmup):
@@ -190,6 +191,7 @@ def run_gpu(args):
             clocks = clocks.stop()
         toks = sum(len(r.tokens) for r in res)
         dev = sum(r.stats["device_s"] for r in res)
+        timed_results[kind] = res
         steps = [s for r in res for s in r.steps]
         results[kind] = dict(tokens=toks, device_s=dev, wall_s=wall, event_s=ev_s,
                              launches=sum(r.stats["launches"] for r in res),
@@ -202,6 +204,7 @@ def run_gpu(args):
     agg = aggregate(results, ws)
     # roofline of the dominant kernel sequence: one target window forward
     rl = roofline(target, draft, args.gamma, args)
+    summary = run_summaries(target, draft, timed_results, args)
     split_model = split_pair_model(target, draft, results["pearl"]["alpha"]) if ws == 1 else None
     target_bytes, draft_bytes = target.cfg.weight_bytes(), draft.cfg.weight_bytes()
     sweep = batch_sweep(target, draft, args, sweep_bs, greedy, temp, ws) if sweep_bs else None
@@ -269,6 +272,7 @@ def run_gpu(args):
         "roofline": rl,
         "split_pair": split,
         "split_pair_model": split_model,
+        "run_summary": summary,
         "batch_sweep": sweep,
         "cpu_baseline": cpu,
         "clocks": clocks,
@@ -278,6 +282,23 @@ def run_gpu(args):
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def run_summaries(target, draft, timed, args):
+    """the CLI's RunSummary (cli.py:65-83, 288-315) of the timed
+    PEARL and SD decodes, each trace priced by the reference's step model
+    (simulator.py) with t and c MEASURED on this GPU, next to the measured
+    speedup -- the simulated-vs-measured comparison and the draft-run
+    histogram (Fig. 2b analogue)."""
+    from paper_2408_11850_b200 import metrics
+    params = metrics.measured_params(target, draft)
+    target.reset_adapter()
+    draft.reset_adapter()
+    out = {"t_draft_ms": round(params.t * 1e3, 4), "c": round(params.c, 2)}
+    for kind in ("pearl", "sd"):
+        if kind in timed:
+            out[kind] = metrics.summarize_run(kind, args.gamma if kind == "sd" else -1, timed[kind], params).to_dict()
+    return out
 
 
 def split_pair_model(target, draft, alpha):
