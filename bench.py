@@ -195,6 +195,7 @@ def run_gpu(args):
         steps = [s for r in res for s in r.steps]
         results[kind] = dict(tokens=toks, device_s=dev, wall_s=wall, event_s=ev_s,
                              launches=sum(r.stats["launches"] for r in res),
+                             replays=sum(r.stats.get("replays", 0) for r in res),
                              mean_tok_per_fwd=pk.mean_tokens_per_target_forward(steps),
                              alpha=pk.empirical_acceptance(steps) if kind != "ar" else None,
                              gamma=res[0].stats.get("gamma"),
@@ -209,7 +210,7 @@ def run_gpu(args):
     target_bytes, draft_bytes = target.cfg.weight_bytes(), draft.cfg.weight_bytes()
     sweep = batch_sweep(target, draft, args, sweep_bs, greedy, temp, ws) if sweep_bs else None
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(target, draft, prompts[0], args, greedy, temp)
     split = None
     if ws >= 2 and ws % 2 == 0 and not args.no_split:
@@ -252,8 +253,12 @@ def run_gpu(args):
                   + ("every forward streams HBM (no flush needed)" if wbytes > 126e6 else "L2-resident (tiny pair)"),
         },
         "e2e": {"value": round(tp / ep, 2), "unit": UNIT,
+                # per decode (one bench step): the prompt ids and the two uniform
+                # tables go up; one step summary (16 + gamma_max + 8 int32)
+                # comes back per step-graph replay
                 "h2d_bytes_per_step": 4 * (args.prompt + 1) + 8 * 2 * 4096,
-                "d2h_bytes_per_step": 4 * 32 * max(1, results["pearl"]["tokens"] // max(1, args.steps))},
+                "d2h_bytes_per_step": int(4 * (16 + args.gamma_max + 8) * results["pearl"]["replays"]
+                                          / max(1, args.steps))},
         "ar_tokens_per_s": round(ta / da, 2),
         "sd_tokens_per_s": round(ts_ / ds_, 2),
         "speedup_vs_ar": round((tp / dp) / (ta / da), 3),
