@@ -258,11 +258,22 @@ class PairRuntime:
         self.seq[:C].copy_(torch.tensor(seq0, dtype=torch.int32))
         st = torch.tensor([C, 0, 0, 0, 0, 0, 0, 0], dtype=torch.int32)
         self.state.copy_(st)
-        # prefill both caches with all but the last committed token
+        # prefill both caches with all but the last committed token; the two
+        # models' prefills are independent (own caches, own position fields)
+        # and run concurrently on their step streams
         if C > 1:
-            self.target.forward(self.seq[:C - 1], C - 1, self.state[S_TPOS:S_TPOS + 1], _FWD_ADVANCE, None)
+            s0 = torch.cuda.current_stream()
+            ts = self.target_stream
+            ts.wait_stream(s0)
+            with torch.cuda.stream(ts):
+                self.target.forward(self.seq[:C - 1], C - 1, self.state[S_TPOS:S_TPOS + 1], _FWD_ADVANCE, None, ts)
             if self.draft is not None:
-                self.draft.forward(self.seq[:C - 1], C - 1, self.state[S_DPOS:S_DPOS + 1], _FWD_ADVANCE, None)
+                ds = self.draft_stream
+                ds.wait_stream(s0)
+                with torch.cuda.stream(ds):
+                    self.draft.forward(self.seq[:C - 1], C - 1, self.state[S_DPOS:S_DPOS + 1], _FWD_ADVANCE, None, ds)
+                s0.wait_stream(ds)
+            s0.wait_stream(ts)
         self.ev[3].record()
         self.ev[3].synchronize()
         if stats is not None:
