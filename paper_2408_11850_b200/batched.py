@@ -201,9 +201,16 @@ class BatchRuntime:
         self.begin_step()
         t, sl, p = self.upload([np.array(toks, np.int32), np.array(slots, np.int32), np.array(pos, np.int32)])
         self.ev[0].record()
-        self.target.forward_slots(t, len(toks), sl, p, None)
-        if self.draft is not None:
-            self.draft.forward_slots(t, len(toks), sl, p, None)
+        main = torch.cuda.current_stream()
+        self.target_stream.wait_stream(main)
+        with torch.cuda.stream(self.target_stream):
+            self.target.forward_slots(t, len(toks), sl, p, None, self.target_stream)
+        if self.draft is not None:  # the two prefills are independent: run them concurrently
+            self.draft_stream.wait_stream(main)
+            with torch.cuda.stream(self.draft_stream):
+                self.draft.forward_slots(t, len(toks), sl, p, None, self.draft_stream)
+            main.wait_stream(self.draft_stream)
+        main.wait_stream(self.target_stream)
         self.ev[1].record()
         self.ev[1].synchronize()
         dt = self.ev[0].elapsed_time(self.ev[1]) / 1e3
