@@ -28,7 +28,6 @@ import os
 import struct
 from typing import Dict, Optional, Tuple
 
-import numpy as np
 import torch
 
 from .llama import LlamaConfig
