@@ -97,6 +97,21 @@ PAIRS = {
 }
 
 
+# alignment knob per pair, calibrated on B200 to alpha-hat ~0.9 at T=1 (tools/calib_alpha.py)
+PAIR_BRANCH_STD = {"llama2-7b/68m": 5e-4, "dsc-33b/1.3b": 1.7e-4, "llama3-70b/8b": 8e-5, "tiny": 2e-4}
+# SMs of the green-context partition PEARL's concurrent draft runs on (the
+# target keeps the rest; 0 = shared SMs; the driver rounds to 8-SM groups).  On
+# its own SMs the 68M draft stops competing with the target's GEMM CTAs for SM
+# slots, and enough of them let it keep up with long draft blocks
+# (tools/green_sweep.sh, current kernels, T=1: PEARL 1165 tok/s at 16-24 SMs,
+# 1285-1295 at 32, 1287-1365 at 40 with gamma 16-32, 1165-1288 at 48; the
+# target's stream-K grid shrinks with it -- AR 307 -> 298 tok/s at 40).
+# DSC-33B/1.3B (prompt 512): shared 130 tok/s, 48 SMs 163 (PEARL > SD on the same
+# model; AR 72.6 -> 66.3 on the 100-SM target).  Llama-3 (V = 128256) needs
+# 16-CTA clusters for its pick / verify, which a partition cannot host: shared SMs.
+PAIR_DRAFT_SMS = {"llama2-7b/68m": 40, "dsc-33b/1.3b": 48, "llama3-70b/8b": 0, "tiny": 0}
+
+
 @dataclass(frozen=True)
 class AlignSpec:
     """Controlled-alignment knobs of a random-init pair (see module doc)."""

@@ -149,7 +149,9 @@ def summarize_run(engine: str, gamma: int, results: Sequence, params: TimingPara
     accepted = sum(tr.accepted_count for tr in steps)
     rejected = sum(1 for tr in steps if tr.correction is not None)
     acceptance = accepted / (accepted + rejected) if accepted + rejected else None
-    hist = Counter(n for r in results for n in draft_run_lengths(r.steps))
+    # cli.py:233-237: runs over all prompts' steps back to back (a run still
+    # open at the end of one prompt continues into the next); none for AR
+    hist = Counter(draft_run_lengths(steps)) if engine != "ar" else Counter()
     walls = [w for w in (walls or []) if w is not None]
     return RunSummary(engine=engine, gamma=gamma, n_prompts=len(results), total_steps=total_steps,
                       total_new_tokens=total_tokens, tokens_per_step=total_tokens / total_steps,
