@@ -366,7 +366,7 @@ def batch_sweep(target, draft, args, bs, greedy, temp, ws):
         row["pearl_vs_sd"] = round(row["pearl"] / row["sd"], 3)
         out[str(B)] = row
     return {"unit": "tokens/s (whole batch, all ranks)", "gammas_tried": list(SWEEP_GAMMAS), "by_batch": out,
-            "note": "lockstep engines; target/draft passes as CUDA graphs, K1 per sequence; B=1 is the "
+            "note": "lockstep engines; target/draft passes as CUDA graphs, one batched K1 launch per step; B=1 is the "
                     "single-sequence graph engine; best fixed gamma per engine"}
 
 

@@ -99,6 +99,37 @@ int pearl_spec_verify(int row_mode, const void* const* p_rows, const void* const
                       int n_uniforms, int32_t* cursor, float inv_temperature, int flags,
                       pearl_verify_result* out, double* accept_probs, void* work, void* stream);
 
+/* One chain of a batched K1 launch (pearl_spec_verify_multi). All pointers
+ * are device pointers. Position i of the chain verifies the id
+ * drafted[i * stride], except that with `tail` non-NULL the last position
+ * (n - 1) reads *tail (a draft pick that never went through the host). */
+typedef struct pearl_verify_chain {
+  const void* const* p_rows;   /* n rows (n + 1 with PEARL_F_BONUS)           */
+  const void* const* q_rows;   /* n rows (ignored with PEARL_F_GREEDY)        */
+  const int32_t* drafted;
+  const int32_t* tail;         /* may be NULL                                 */
+  const double* uniforms;      /* this chain's verify stream (NULL if greedy) */
+  int32_t* cursor;             /* its device cursor (may be NULL)             */
+  pearl_verify_result* out;
+  void* work;                  /* pearl_verify_work_bytes(n), zeroed once     */
+  int32_t n;
+  int32_t cluster_base;        /* sum over the previous chains of n (+1 with PEARL_F_BONUS) */
+  int32_t stride;
+  int32_t reserved;
+} pearl_verify_chain;
+
+/*
+ * K1 over many independent chains in ONE launch: the B sequences of a
+ * lockstep batch, each with its own rows, drafted ids,
+ * uniform stream, cursor, verdict and work buffer. Chain s is exactly
+ * pearl_spec_verify on its own arguments (bit-identical verdicts), its
+ * positions running as clusters cluster_base .. cluster_base + n (+1) - 1.
+ * `chains`: device array of n_chains descriptors sorted by cluster_base;
+ * n_clusters = the sum of all chains' cluster counts.
+ */
+int pearl_spec_verify_multi(int row_mode, const pearl_verify_chain* chains, int n_chains, int n_clusters,
+                            int V, int n_uniforms, float inv_temperature, int flags, void* stream);
+
 /*
  * Inverse-CDF / argmax pick from `rows` rows of one law each.
  * Replaces core.sample (core.py:182-190) and engines._pick (engines.py:214-217).

@@ -55,6 +55,7 @@ SIGNATURES = {
                                  _vp, _vp]),
     "pearl_sample_rows": (_i32, [_i32, _vp, _i32, _i32, _vp, _i32, _vp, _f32, _i32, _vp, _vp, _vp, _vp,
                                  _vp]),
+    "pearl_spec_verify_multi": (_i32, [_i32, _vp, _i32, _i32, _i32, _i32, _f32, _i32, _vp]),
     "pearl_sample_rows_multi": (_i32, [_i32, _vp, _i32, _i32, _vp, _i32, _vp, _f32, _i32, _vp, _vp, _vp]),
     "pearl_logits_to_probs": (_i32, [_vp, _i32, _i32, _f32, _vp, _vp, _vp]),
     "pearl_residual": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp]),

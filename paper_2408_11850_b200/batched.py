@@ -13,8 +13,10 @@ advance in lockstep and share every model pass:
   (plus the catch-up tokens after a rejection), followed by one
   ``pearl_sample_rows_multi`` launch that picks every sequence's next draft
   from its own uniform stream;
-* verification is K1 per sequence (its own chain length, uniform stream and
-  verdict), then the host applies each sequence's PRE / POST transition.
+* verification is ONE K1 launch for all sequences
+  (``pearl_spec_verify_multi``: each chain its own length, rows, uniform
+  stream, cursor and verdict; the last draft id read on the device), then the
+  host applies each sequence's PRE / POST transition.
 
 Each sequence keeps exactly the state machine of the single-sequence engines
 (engines.py:397-526 for PEARL, :344-394 SD, :289-319 AR), its own split
@@ -91,7 +93,6 @@ class BatchRuntime:
         self.qbuf = torch.zeros(2, g + 1, B, V, dtype=torch.float32, device=dev)
         self.trows = torch.zeros(B * (g + 2), V, dtype=torch.float32, device=dev)
         self.xs = torch.zeros(g + 1, B, **i32)
-        self.chain = torch.zeros(B, 2 * g + 2, **i32)
         self.verdict = torch.zeros(B, 8, **i32)
         self.status = torch.zeros(1, **i32)
         wb = int(self.lib.pearl_verify_work_bytes(g + 2))
@@ -100,7 +101,7 @@ class BatchRuntime:
         # (sized for the largest upload: a prefill of every slot's full context)
         self.ibuf = torch.zeros(2 * B * self.max_len + 16 * B * (g + 2) * (g + 2) + 4096, dtype=torch.int64, device=dev)
         self.ibuf_host = torch.zeros_like(self.ibuf, device="cpu").pin_memory()
-        self.out_host = torch.zeros(B * 8 + (g + 1) * B + 2 * B, dtype=torch.int32).pin_memory()
+        self.out_host = torch.zeros(B * 8 + (g + 1) * B + 2 * B + 1, dtype=torch.int32).pin_memory()
         self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         self.draft_stream = torch.cuda.Stream(device=dev)
         self.target_stream = torch.cuda.Stream(device=dev)
@@ -165,14 +166,21 @@ class BatchRuntime:
             _lib.ROWS_LOGITS32, _device.ptr(rows_ptrs), n, self.V, _device.ptr(sptrs), U_TABLE, _addr(sptrs, n),
             invt, flags, out_addr, _device.ptr(self.status), _device.stream_ptr(stream)), "pick (batched)")
 
-    def verify(self, i: int, p_ptrs: torch.Tensor, q_ptrs: Optional[torch.Tensor], n: int, invt: float,
-               greedy: bool, bonus: bool, stream) -> None:
+    def chain_desc(self, r_slot: int, p_addr: int, q_addr: int, drafted: int, tail: int, stride: int, n: int,
+                   base: int) -> np.ndarray:
+        """One pearl_verify_chain descriptor (include/pearl_b200.h) as 10 int64 words."""
+        return np.array([p_addr, q_addr, drafted, tail, int(self.tables[1, r_slot].data_ptr()),
+                         _addr(self.cursors[1], r_slot), _addr(self.verdict[r_slot]), _addr(self.work[r_slot]),
+                         n | (base << 32), stride], np.int64)
+
+    def verify_multi(self, d: torch.Tensor, n_chains: int, n_clusters: int, invt: float, greedy: bool, bonus: bool,
+                     stream) -> None:
+        """K1 for every active sequence in one launch (pearl_spec_verify_multi);
+        `d` = the uploaded chain_desc words."""
         flags = (_lib.F_GREEDY if greedy else 0) | _lib.F_ADVANCE | (_lib.F_BONUS if bonus else 0)
-        _lib.check(self.lib.pearl_spec_verify(
-            _lib.ROWS_LOGITS32, _device.ptr(p_ptrs), _device.ptr(q_ptrs), _device.ptr(self.chain[i]), n, self.V,
-            _device.ptr(self.tables[1, i]), U_TABLE, _addr(self.cursors[1], i), invt, flags,
-            _device.ptr(self.verdict[i]), None, _device.ptr(self.work[i]), _device.stream_ptr(stream)),
-            "spec_verify (batched)")
+        _lib.check(self.lib.pearl_spec_verify_multi(
+            _lib.ROWS_LOGITS32, _device.ptr(d), n_chains, n_clusters, self.V, U_TABLE, invt, flags,
+            _device.stream_ptr(stream)), "spec_verify_multi (batched)")
 
     def replay(self, key: tuple, fn, stream) -> None:
         """Run fn(stream) as a CUDA graph keyed by its shape (captured on first use)."""
@@ -323,13 +331,16 @@ def _read_back(rt: BatchRuntime, n: int, gamma: int) -> tuple:
     h = rt.out_host
     h[:B * 8].copy_(rt.verdict.view(-1), non_blocking=True)
     h[B * 8:B * 8 + (rt.g + 1) * B].copy_(rt.xs.view(-1), non_blocking=True)
-    h[B * 8 + (rt.g + 1) * B:].copy_(rt.cursors.view(-1), non_blocking=True)
+    c0 = B * 8 + (rt.g + 1) * B
+    h[c0:c0 + 2 * B].copy_(rt.cursors.view(-1), non_blocking=True)
+    h[c0 + 2 * B:].copy_(rt.status, non_blocking=True)
     rt.ev[1].record()
     rt.ev[1].synchronize()
     a = h.numpy()
     verdict = a[:B * 8].reshape(B, 8)
-    xs = a[B * 8:B * 8 + (rt.g + 1) * B].reshape(rt.g + 1, B)
-    cur = a[B * 8 + (rt.g + 1) * B:].reshape(2, B)
+    xs = a[B * 8:c0].reshape(rt.g + 1, B)
+    cur = a[c0:c0 + 2 * B].reshape(2, B)
+    _lib.check(int(a[c0 + 2 * B]), "pick (batched)")
     return verdict, xs, cur
 
 
@@ -387,8 +398,20 @@ def decode_pearl_batch(draft: LlamaModel, target: LlamaModel, prompts: Sequence[
             k = len(s.pending)
             ptr_rows.append(np.array([rt.row(rt.trows, offs[r] + j) for j in range(k + 1)]
                                      + s.pending_q + [q0[r]], np.int64))
-        flat = rt.upload([np.concatenate(ptr_rows)] + [np.array(s.pending, np.int32) for s in act if s.pending])
-        ptrs, pend = flat[0], flat[1:]
+        pend_all = [t for s in act for t in s.pending]
+        ptrs, pend = rt.upload([np.concatenate(ptr_rows), np.array(pend_all or [0], np.int32)])
+        # chains = pending + [x_0] (x_0 read on the device): one K1 launch for all sequences
+        descs, off, poff, base = [], 0, 0, 0
+        for r, s in enumerate(act):
+            k = len(s.pending)
+            pa = _addr(ptrs, off)
+            x0 = _addr(rt.xs[0], r)
+            descs.append(rt.chain_desc(s.slot, pa, pa + 8 * (k + 1), _addr(pend, poff) if k else x0, x0, 1, k + 1,
+                                       base))
+            off += 2 * k + 2
+            poff += k
+            base += k + 1
+        (dd,) = rt.upload([np.concatenate(descs)])
         rt.draft_stream.wait_stream(main)
         rt.target_stream.wait_stream(main)
         nt = len(ttok)
@@ -396,22 +419,10 @@ def decode_pearl_batch(draft: LlamaModel, target: LlamaModel, prompts: Sequence[
         _draft_launch(rt, prep, n, gamma, par, invt, greedy, rt.draft_stream)
         main.wait_stream(rt.draft_stream)
         main.wait_stream(rt.target_stream)
-        # chains = pending + [x_0]; K1 per sequence
-        pi = 0
-        off = 0
-        for r, s in enumerate(act):
-            k = len(s.pending)
-            if k:
-                rt.chain[s.slot, :k].copy_(pend[pi])
-                pi += 1
-            rt.chain[s.slot, k].copy_(rt.xs[0, r])
-            rt.verify(s.slot, ptrs[off:off + k + 1], ptrs[off + k + 1:off + 2 * k + 2], k + 1, invt, greedy, False,
-                      main)
-            off += 2 * k + 2
+        rt.verify_multi(dd, n, base, invt, greedy, False, main)
         verdict, xs_h, cur = _read_back(rt, n, gamma)
         stats["device_s"] += rt.ev[0].elapsed_time(rt.ev[1]) / 1e3
         stats["steps"] += 1
-        _lib.check(int(rt.status.item()), "pick (batched)")
         for r, s in enumerate(act):
             v = verdict[s.slot]
             _lib.check(int(v[0]), "decode_pearl_batch step")
@@ -486,22 +497,24 @@ def decode_sd_batch(draft: LlamaModel, target: LlamaModel, prompts: Sequence[Seq
                                      + [q0[r]] + [rt.row(rt.qbuf[0, j], r) for j in range(1, gamma)], np.int64))
         ts, tp, ff, ptrs = rt.upload([np.array(tslot, np.int32), np.array(tpos, np.int32), np.array(first, np.int32),
                                       np.concatenate(ptr_rows)])
+        # chain r = xs[:gamma, r] (stride B in rt.xs), bonus row p_gamma: one K1 launch
+        descs, off = [], 0
+        for r, s in enumerate(act):
+            pa = _addr(ptrs, off)
+            descs.append(rt.chain_desc(s.slot, pa, pa + 8 * (gamma + 1), _addr(rt.xs[0], r), 0, rt.B, gamma,
+                                       r * (gamma + 1)))
+            off += 2 * gamma + 1
+        (dd,) = rt.upload([np.concatenate(descs)])
         _draft_launch(rt, prep, n, gamma, 0, invt, greedy, main)
         # window ids: [first_r, xs[0][r], .., xs[gamma-1][r]] per sequence, gathered on the device
         tt = torch.empty((n, gamma + 1), dtype=torch.int32, device=rt.dev)
         tt[:, 0] = ff
         tt[:, 1:] = rt.xs[:gamma, :n].t()
         target.forward_slots(tt.view(-1), n * (gamma + 1), ts, tp, rt.trows, main)
-        off = 0
-        for r, s in enumerate(act):
-            rt.chain[s.slot, :gamma].copy_(rt.xs[:gamma, r])
-            rt.verify(s.slot, ptrs[off:off + gamma + 1], ptrs[off + gamma + 1:off + 2 * gamma + 1], gamma, invt,
-                      greedy, True, main)
-            off += 2 * gamma + 1
+        rt.verify_multi(dd, n, n * (gamma + 1), invt, greedy, True, main)
         verdict, xs_h, cur = _read_back(rt, n, gamma)
         stats["device_s"] += rt.ev[0].elapsed_time(rt.ev[1]) / 1e3
         stats["steps"] += 1
-        _lib.check(int(rt.status.item()), "pick (batched)")
         for r, s in enumerate(act):
             v = verdict[s.slot]
             _lib.check(int(v[0]), "decode_sd_batch step")

@@ -272,15 +272,32 @@ struct VerifyArgs {
   double* accept_out;
 };
 
-__global__ void __launch_bounds__(kThreads) spec_verify_kernel(VerifyArgs A) {
-  cg::cluster_group cl = cg::this_cluster();
-  ClusterCtx cc{static_cast<int>(cl.block_rank()), static_cast<int>(cl.num_blocks()), 0};
-  const int pos = blockIdx.x / cc.size;
-  int* plan = reinterpret_cast<int*>(g_smem);
-  Scratch& s = *reinterpret_cast<Scratch*>(g_smem + kPlanStride * sizeof(int));
-  double* P = reinterpret_cast<double*>(g_smem + kPlanStride * sizeof(int) + sizeof(Scratch));
-  double* Q = P + A.job.cap;
-  load_plan(plan, A.job.plan, cc.rank);
+// one chain as the verify body sees it (a pearl_spec_verify call, or one
+// descriptor of a pearl_spec_verify_multi launch)
+struct ChainView {
+  RowJob job;
+  int flags;
+  int n;
+  const void* const* p_rows;
+  const void* const* q_rows;
+  const int32_t* drafted;
+  const int32_t* tail;
+  int stride;
+  const double* uniforms;
+  int n_uniforms;
+  int32_t* cursor;
+  WorkHdr* work;
+  pearl_verify_result* out;
+  double* accept_out;
+  __device__ __forceinline__ int id(int pos) const {
+    return (tail != nullptr && pos == n - 1) ? *tail : drafted[pos * stride];
+  }
+};
+
+// position `pos` of chain A on this cluster; the chain's last-arriving
+// cluster reduces the verdict (first reject by ballot) and advances its cursor
+__device__ __forceinline__ void verify_position(ClusterCtx& cc, const int* plan, Scratch& s, double* P,
+                                                double* Q, const ChainView& A, int pos) {
   const int lo = plan[3];
   const bool greedy = (A.flags & PEARL_F_GREEDY) != 0;
   const bool probe = (A.flags & PEARL_F_PROBE) != 0;
@@ -309,7 +326,7 @@ __global__ void __launch_bounds__(kThreads) spec_verify_kernel(VerifyArgs A) {
       }
     }
   } else {
-    const int x = A.drafted[pos];
+    const int x = A.id(pos);
     const void* rows[2] = {A.p_rows[pos], A.q_rows[pos]};
     double* sl[2] = {P, Q};
     RowNorm nm[2];
@@ -445,6 +462,62 @@ __global__ void __launch_bounds__(kThreads) spec_verify_kernel(VerifyArgs A) {
   *A.out = res;
   if (A.cursor && (A.flags & PEARL_F_ADVANCE) && res.status == PEARL_OK) *A.cursor = cur + res.draws_used;
   A.work->arrived = 0;
+}
+
+__device__ __forceinline__ void verify_smem(const RowJob& job, int*& plan, Scratch*& s, double*& P, double*& Q) {
+  plan = reinterpret_cast<int*>(g_smem);
+  s = reinterpret_cast<Scratch*>(g_smem + kPlanStride * sizeof(int));
+  P = reinterpret_cast<double*>(g_smem + kPlanStride * sizeof(int) + sizeof(Scratch));
+  Q = P + job.cap;
+}
+
+__global__ void __launch_bounds__(kThreads) spec_verify_kernel(VerifyArgs A) {
+  cg::cluster_group cl = cg::this_cluster();
+  ClusterCtx cc{static_cast<int>(cl.block_rank()), static_cast<int>(cl.num_blocks()), 0};
+  int* plan;
+  Scratch* s;
+  double *P, *Q;
+  verify_smem(A.job, plan, s, P, Q);
+  load_plan(plan, A.job.plan, cc.rank);
+  const ChainView v{A.job, A.flags, A.n, A.p_rows, A.q_rows, A.drafted, nullptr, 1, A.uniforms, A.n_uniforms,
+                    A.cursor, A.work, A.out, A.accept_out};
+  verify_position(cc, plan, *s, P, Q, v, blockIdx.x / cc.size);
+}
+
+static_assert(sizeof(pearl_verify_chain) == 80, "pearl_verify_chain layout (batched.py packs it)");
+
+struct VerifyMultiArgs {
+  RowJob job;
+  int flags;
+  int n_chains;
+  int n_uniforms;
+  const pearl_verify_chain* chains;
+};
+
+__global__ void __launch_bounds__(kThreads) spec_verify_multi_kernel(VerifyMultiArgs A) {
+  cg::cluster_group cl = cg::this_cluster();
+  ClusterCtx cc{static_cast<int>(cl.block_rank()), static_cast<int>(cl.num_blocks()), 0};
+  int* plan;
+  Scratch* s;
+  double *P, *Q;
+  verify_smem(A.job, plan, s, P, Q);
+  load_plan(plan, A.job.plan, cc.rank);
+  const int c = blockIdx.x / cc.size;
+  __shared__ int s_chain;
+  // chain of cluster c = (number of chains with cluster_base <= c) - 1 (sorted bases)
+  if (threadIdx.x < 32) {
+    int cnt = 0;
+    for (int b = 0; b < A.n_chains; b += 32) {
+      const int i = b + threadIdx.x;
+      cnt += __popc(__ballot_sync(0xffffffffu, i < A.n_chains && A.chains[i].cluster_base <= c));
+    }
+    if (threadIdx.x == 0) s_chain = cnt - 1;
+  }
+  __syncthreads();
+  const pearl_verify_chain& d = A.chains[s_chain];
+  const ChainView v{A.job, A.flags, d.n, d.p_rows, d.q_rows, d.drafted, d.tail, d.stride, d.uniforms,
+                    d.uniforms ? A.n_uniforms : 0, d.cursor, static_cast<WorkHdr*>(d.work), d.out, nullptr};
+  verify_position(cc, plan, *s, P, Q, v, c - d.cluster_base);
 }
 
 // ---------------------------------------------------------------------------
@@ -635,6 +708,7 @@ int configure_all() {
     // worst case slice: V=131072 over 16 CTAs -> 8192 (+ rounding) elements, 2 slices
     const size_t smem = kPlanStride * sizeof(int) + sizeof(Scratch) + 2 * 8320 * sizeof(double);
     int st = configure(spec_verify_kernel, smem);
+    if (st == PEARL_OK) st = configure(spec_verify_multi_kernel, smem);
     if (st == PEARL_OK) st = configure(sample_rows_kernel, smem);
     if (st == PEARL_OK) st = configure(logits_to_probs_kernel, smem);
     if (st == PEARL_OK) st = configure(residual_kernel, smem);
@@ -693,6 +767,26 @@ extern "C" int pearl_spec_verify(int row_mode, const void* const* p_rows, const 
   a.accept_out = accept_probs;
   const int clusters = n + ((flags & PEARL_F_BONUS) ? 1 : 0);
   return launch_clustered(spec_verify_kernel, clusters, plan->C, smem_bytes(*plan, 2), stream, a);
+}
+
+extern "C" int pearl_spec_verify_multi(int row_mode, const pearl_verify_chain* chains, int n_chains,
+                                       int n_clusters, int V, int n_uniforms, float inv_temperature, int flags,
+                                       void* stream) {
+  PEARL_ARG_CHECK(n_chains >= 1 && n_clusters >= n_chains, "need at least one chain of one position");
+  PEARL_ARG_CHECK(row_mode == PEARL_ROWS_PROBS64 || row_mode == PEARL_ROWS_LOGITS32, "bad row mode");
+  PEARL_ARG_CHECK(chains != nullptr, "null argument");
+  PEARL_ARG_CHECK(inv_temperature > 0.0f, "inverse temperature must be positive");
+  int st = configure_all();
+  if (st != PEARL_OK) return st;
+  const VocabPlan* plan = get_plan(V);
+  if (!plan) return PEARL_ERR_ARG;
+  VerifyMultiArgs a{};
+  a.job = RowJob{row_mode, inv_temperature, V, plan->d_plan, plan->cap};
+  a.flags = flags;
+  a.n_chains = n_chains;
+  a.n_uniforms = n_uniforms;
+  a.chains = chains;
+  return launch_clustered(spec_verify_multi_kernel, n_clusters, plan->C, smem_bytes(*plan, 2), stream, a);
 }
 
 extern "C" int pearl_sample_rows(int row_mode, const void* const* rows, int n_rows, int V,

@@ -237,3 +237,73 @@ def test_large_vocab_against_oracle(pk, V):
                                              _device.stream_ptr()))
     assert int(st.item()) == 0
     assert out.cpu().tolist() == [sample_index(cdf, x) for x in us]
+
+
+def _verify_multi(chains, V, flags, mode=0, inv_t=1.0, tail=False):
+    """pearl_spec_verify_multi over `chains` = [(P rows, Q rows or None, drafted, uniforms)] in ONE
+    launch; with tail=True each chain's last id is read through the descriptor's tail pointer."""
+    from paper_2408_11850_b200 import _device, _lib
+    dev = torch.device("cuda")
+    _lib.prepare_vocab(V)
+    bonus = bool(flags & _lib.F_BONUS)
+    keep, words, base = [], [], 0
+    wb = int(_lib.load().pearl_verify_work_bytes(max(len(c[2]) for c in chains) + 1))
+    outs = torch.zeros(len(chains), 8, dtype=torch.int32, device=dev)
+    curs = torch.zeros(len(chains), dtype=torch.int32, device=dev)
+    work = torch.zeros(len(chains), wb, dtype=torch.uint8, device=dev)
+    for i, (P, Q, drafted, us) in enumerate(chains):
+        pr = _device.row_ptrs(P, dev)
+        qr = _device.row_ptrs(Q, dev) if Q else pr
+        ids = list(drafted) + [-7]  # a poisoned slot after the chain
+        if tail:
+            ids[len(drafted) - 1] = -5  # must be read through `tail` instead
+        toks = torch.tensor(ids, dtype=torch.int32, device=dev)
+        tl = torch.tensor([drafted[-1]], dtype=torch.int32, device=dev)
+        u = torch.tensor(np.asarray(us, dtype=np.float64), device=dev) if len(us) else None
+        keep += [pr, qr, toks, tl, u]
+        n = len(drafted)
+        words.append([pr.data_ptr(), qr.data_ptr(), toks.data_ptr(), tl.data_ptr() if tail else 0,
+                      0 if u is None else u.data_ptr(), curs[i:].data_ptr(), outs[i].data_ptr(),
+                      work[i].data_ptr(), n | (base << 32), 1])
+        base += n + (1 if bonus else 0)
+    d = torch.tensor(np.array(words, np.int64).reshape(-1), device=dev)
+    n_u = max(len(c[3]) for c in chains)
+    _lib.check(_lib.load().pearl_spec_verify_multi(mode, _device.ptr(d), len(chains), base, V, n_u, inv_t,
+                                                   flags | _lib.F_ADVANCE, _device.stream_ptr()))
+    torch.cuda.synchronize()
+    o = outs.cpu().numpy()
+    c = curs.cpu().numpy()
+    return [dict(status=int(r[0]), accepted=int(r[1]), correction=int(r[2]), examined=int(r[3]), draws=int(r[4]),
+                 bonus=int(r[5]), cursor=int(ci)) for r, ci in zip(o, c)]
+
+
+def test_verify_multi_equals_per_chain(pk):
+    """One batched K1 launch == pearl_spec_verify per chain (golden verdicts), mixed
+    chain lengths, sampled / greedy / SD bonus, ids via the tail pointer."""
+    from paper_2408_11850_b200 import _lib
+    g = load_golden("verify_cases.json")
+    by_v = {}
+    for case in g["cases"]:
+        by_v.setdefault(case["V"], []).append(case)
+    for V, cases in by_v.items():
+        cases = cases[:12]
+        chains, singles = [], []
+        for case in cases:
+            ps, qs = recipes.make_rows(case["V"], case["n"], case["seed"], case["kind"])
+            P, Q = _probs_rows(ps), _probs_rows(qs)
+            us = pk.RandomStream(case["seed"] + case["rng_seed"]).split(1).peek(case["n"] + 2)
+            chains.append((P, Q, case["drafted"], us))
+            singles.append((0, case["accepted"], case["correction"], case["examined"], case["n_draws"]))
+        for tail in (False, True):
+            got = _verify_multi(chains, V, 0, tail=tail)
+            assert [(r["status"], r["accepted"], r["correction"], r["examined"], r["draws"]) for r in got] == singles
+            assert [r["cursor"] for r in got] == [s[4] for s in singles]
+        got = _verify_multi([(P, None, d, []) for P, _, d, _ in chains], V, _lib.F_GREEDY)
+        assert [(r["accepted"], r["correction"]) for r in got] == [(c["g_accepted"], c["g_correction"]) for c in cases]
+        # SD bonus: p has one more row; compare with the single-chain kernel on the same rows
+        bon = [(P + [P[0]], Q, d, us) for P, Q, d, us in chains]
+        got = _verify_multi(bon, V, _lib.F_BONUS)
+        for (P, Q, d, us), r in zip(bon, got):
+            want = _verify(pk, P, Q, d, us, flags=_lib.F_BONUS)
+            assert (r["status"], r["accepted"], r["correction"], r["bonus"], r["draws"]) == (
+                want["status"], want["accepted"], want["correction"], want["bonus"], want["draws"])
