@@ -689,7 +689,7 @@ def main():
     ap.add_argument("--cpu-prompt", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-split", action="store_true", help="N>=2: skip the split-pair (draft GPU / target GPU) leg")
-    ap.add_argument("--batch-sweep", default="1,4,16",
+    ap.add_argument("--batch-sweep", default="1,4,16,32",
                     help="C5: comma-separated batch sizes decoded in lockstep (empty string: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
