@@ -378,9 +378,9 @@ void tc_free(TcGemmCtx& ctx) {
 }
 
 int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int M, int N, int K, const EpiArgs& e,
-            cudaStream_t st, int force_splits, TcNext next) {
+            cudaStream_t st, int force_splits) {
   if (M < 1 || M > kMaxTokTiles * kTokTile) {
-    set_error("tc_gemm: M must be in [1, 64]");
+    set_error("tc_gemm: M must be in [1, 128]");
     return PEARL_ERR_ARG;
   }
   if (K % 8 != 0) {
@@ -410,7 +410,6 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.e = e;
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;
-  (void)next;  // (L2 prefetch of the next GEMM's weights: measured slower, profiles/README.md)
   if (static_cast<size_t>(tiles) * a.seg_max * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
       tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");

@@ -40,14 +40,8 @@ struct TcGemmCtx {
 
 int tc_init(TcGemmCtx& ctx, const pearl_llama_config& cfg);
 void tc_free(TcGemmCtx& ctx);
-// The GEMM that follows in the forward (its weights are prefetched into L2
-// during this GEMM's tail; W == nullptr: none).
-struct TcNext {
-  const __nv_bfloat16* W = nullptr;
-  int N = 0, K = 0;
-};
 int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int M, int N, int K,
-            const EpiArgs& e, cudaStream_t st, int force_grid = 0, TcNext next = TcNext{});
+            const EpiArgs& e, cudaStream_t st, int force_grid = 0);
 // number of K splits the (legacy round-robin) planner picks for an (N, K) GEMM
 int tc_splits(int N, int K, int num_sms);
 // most stream-K segments any tile of an (tiles x KB) GEMM is cut into over G CTAs

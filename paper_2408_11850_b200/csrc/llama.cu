@@ -594,9 +594,9 @@ int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs
 
 static int ablate_mask();
 int launch_gemm(Llama& m, const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
-                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}, TcNext next = TcNext{}) {
+                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
   if (ablate_mask() & 4) return PEARL_OK;
-  if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st, 0, next);
+  if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st, 0);
   return launch_gemv(W, X, M, N, K, e, st, nrm);
 }
 
@@ -708,8 +708,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     e.n_kv = nkv;
     e.hd = hd;
     rc = launch_gemm(m, L.wqkv, m.x, M, nq + 2 * nkv, d, e, st,
-                     fuse_norm ? GemvNorm{m.h, L.attn_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f},
-                     TcNext{L.wo, d, nq});
+                     fuse_norm ? GemvNorm{m.h, L.attn_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
     if (rc) return rc;
     g_prof.mark(OP_QKV, st);
   if (halt()) return PEARL_OK;
@@ -730,7 +729,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     r.kind = EPI_RESID;
     r.out_f32 = m.h;
     r.ld = d;
-    rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st, GemvNorm{nullptr, nullptr, 0.f}, TcNext{L.wgu, 2 * c.ffn, d});
+    rc = launch_gemm(m, L.wo, m.o, M, d, nq, r, st);
     if (rc) return rc;
     g_prof.mark(OP_O, st);
   if (halt()) return PEARL_OK;
@@ -745,14 +744,11 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     g.out_bf16 = m.act;
     g.ld = c.ffn;
     rc = launch_gemm(m, L.wgu, m.x, M, 2 * c.ffn, d, g, st,
-                     fuse_norm ? GemvNorm{m.h, L.mlp_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f},
-                     TcNext{L.wdown, d, c.ffn});
+                     fuse_norm ? GemvNorm{m.h, L.mlp_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
     if (rc) return rc;
     g_prof.mark(OP_GU, st);
   if (halt()) return PEARL_OK;
-    const TcNext after_down = l + 1 < c.n_layers ? TcNext{m.layers[l + 1].wqkv, nq + 2 * nkv, d}
-                              : (want_logits ? TcNext{m.lm_head, c.vocab, d} : TcNext{});
-    rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r, st, GemvNorm{nullptr, nullptr, 0.f}, after_down);
+    rc = launch_gemm(m, L.wdown, m.act, M, d, c.ffn, r, st);
     if (rc) return rc;
     g_prof.mark(OP_DOWN, st);
   if (halt()) return PEARL_OK;
