@@ -167,6 +167,8 @@ def parse_run_config(doc: dict) -> RunConfig:
     engine = doc["engine"]
     if engine in ("sd", "pearl") and "gamma" not in doc:
         raise ConfigError("$.gamma", f"engine {engine!r} requires gamma")
+    if doc.get("batch", 1) > 1 and doc.get("adaptive_gamma", False):
+        raise ConfigError("$.adaptive_gamma", "batched (lockstep) decoding drafts a fixed gamma")
     if "prompts" in doc and "synthetic_prompts" in doc:
         raise ConfigError("$.synthetic_prompts", "give either prompts or synthetic_prompts")
     timing = TimingParams(t=doc["timing"]["t"], c=doc["timing"]["c"]) if "timing" in doc else None

@@ -66,6 +66,7 @@ def _doc(**over):
     (_doc(model={"synthetic": {"alpha": 0.5}, "transformer": {"arch": "tiny"}}), "$.model"),
     (_doc(prompts="p.txt", synthetic_prompts={"n": 1, "length": 4, "seed": 0}), "$.synthetic_prompts"),
     (_doc(timing={"t": 0, "c": 2}), "$.timing.t"),
+    (_doc(batch=4, adaptive_gamma=True), "$.adaptive_gamma"),
 ])
 def test_config_errors_carry_json_path(doc, path):
     from paper_2408_11850_b200 import runconfig
