@@ -333,6 +333,7 @@ def batch_sweep(target, draft, args, bs, greedy, temp, ws):
     import torch
     import paper_2408_11850_b200 as pk
     from paper_2408_11850_b200 import batched
+    sweep_gammas = [int(g) for g in args.sweep_gammas.split(",")] if args.sweep_gammas else list(SWEEP_GAMMAS)
     out = {}
     V = target.cfg.vocab
     for B in bs:
@@ -348,7 +349,7 @@ def batch_sweep(target, draft, args, bs, greedy, temp, ws):
             return ws * toks / res[0].stats["device_s"], steps
         for kind in ("pearl", "sd"):
             best = None
-            for g in SWEEP_GAMMAS:
+            for g in sweep_gammas:
                 cfg = pk.EngineConfig(gamma=g, max_new_tokens=args.new, seed=29, greedy=greedy, temperature=temp,
                                       gamma_max=max(g, args.gamma_max))
                 fn = (lambda c=cfg: batched.decode_pearl_batch(draft, target, prompts, c)) if kind == "pearl" else \
@@ -365,7 +366,7 @@ def batch_sweep(target, draft, args, bs, greedy, temp, ws):
         row["pearl_vs_ar"] = round(row["pearl"] / row["ar"], 3)
         row["pearl_vs_sd"] = round(row["pearl"] / row["sd"], 3)
         out[str(B)] = row
-    return {"unit": "tokens/s (whole batch, all ranks)", "gammas_tried": list(SWEEP_GAMMAS), "by_batch": out,
+    return {"unit": "tokens/s (whole batch, all ranks)", "gammas_tried": list(sweep_gammas), "by_batch": out,
             "note": "lockstep engines; target/draft passes as CUDA graphs, one batched K1 launch per step; B=1 is the "
                     "single-sequence graph engine; best fixed gamma per engine"}
 
@@ -689,6 +690,8 @@ def main():
     ap.add_argument("--cpu-prompt", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-split", action="store_true", help="N>=2: skip the split-pair (draft GPU / target GPU) leg")
+    ap.add_argument("--sweep-gammas", default=",".join(str(g) for g in SWEEP_GAMMAS),
+                    help="C5: fixed draft lengths tried per engine and batch size")
     ap.add_argument("--batch-sweep", default="1,4,16,32",
                     help="C5: comma-separated batch sizes decoded in lockstep (empty string: skip)")
     args = ap.parse_args()
