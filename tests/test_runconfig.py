@@ -140,3 +140,43 @@ def test_transformer_run_on_device(tmp_path, engine):
     js = json.loads((tmp_path / "b1" / "run_summary.json").read_text())
     assert js["engine"] == engine and js["total_new_tokens"] == 72
     assert timing.c > 1.0  # measured on the GPU: the target forward costs more than the draft's
+
+
+@pytest.mark.gpu
+def test_transformer_checkpoint_run(tmp_path):
+    """``checkpoint`` instead of ``arch``: Hugging Face safetensors for target and
+    draft (checkpoint.load_llama) decoded end to end from a run config."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2408_11850_b200 import checkpoint, runconfig
+    d, F, V = 256, 512, 1024
+    for name, seed, layers in (("target", 1, 2), ("draft", 2, 1)):
+        g = torch.Generator().manual_seed(seed)
+
+        def r(*s, std=0.05):
+            return (torch.randn(*s, generator=g) * std).to(torch.bfloat16)
+        t = {"model.embed_tokens.weight": r(V, d, std=1.0), "model.norm.weight": torch.ones(d),
+             "lm_head.weight": r(V, d)}
+        for i in range(layers):
+            p = f"model.layers.{i}."
+            for n, shape in (("self_attn.q_proj", (256, d)), ("self_attn.k_proj", (128, d)),
+                             ("self_attn.v_proj", (128, d)), ("self_attn.o_proj", (d, 256)),
+                             ("mlp.gate_proj", (F, d)), ("mlp.up_proj", (F, d)), ("mlp.down_proj", (d, F))):
+                t[p + n + ".weight"] = r(*shape)
+            t[p + "input_layernorm.weight"] = torch.ones(d)
+            t[p + "post_attention_layernorm.weight"] = torch.ones(d)
+        (tmp_path / name).mkdir()
+        checkpoint.write_safetensors(str(tmp_path / name / "model.safetensors"), t)
+        (tmp_path / name / "config.json").write_text(json.dumps(
+            {"num_hidden_layers": layers, "hidden_size": d, "num_attention_heads": 4, "num_key_value_heads": 2,
+             "intermediate_size": F, "vocab_size": V}))
+    (tmp_path / "p.txt").write_text("5 17 300 9\n900 31 2\n")
+    doc = {"engine": "pearl", "gamma": 3, "max_new_tokens": 20, "seed": 4, "prompts": str(tmp_path / "p.txt"),
+           "model": {"transformer": {"checkpoint": {"target": str(tmp_path / "target"),
+                                                    "draft": str(tmp_path / "draft")}}}}
+    (tmp_path / "cfg.json").write_text(json.dumps(doc))
+    assert runconfig.main(["run", "--config", str(tmp_path / "cfg.json"), "--out", str(tmp_path / "o")]) == 0
+    out = (tmp_path / "o" / "outputs.txt").read_text().splitlines()
+    assert len(out) == 2 and all(len(line.split()) == 20 for line in out)
+    assert all(0 <= int(x) < V for line in out for x in line.split())
