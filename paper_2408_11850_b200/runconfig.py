@@ -21,8 +21,9 @@ Model families:
   ([target, draft]; one GPU in process -- a draft on another GPU is the split
   pair, split_pair.connect_pair, one process per GPU), ``gemm``,
   ``draft_sms``, ``temperature``, ``eos_id``.  Prompts are token ids: one
-  prompt per line of ``prompts`` (whitespace-separated ints) or
-  ``synthetic_prompts`` {"n", "length", "seed"}.  ``timing`` is optional and
+  prompt per line of ``prompts`` (whitespace-separated ints; an empty line, or
+  no prompts at all, decodes from BOS alone, like the reference's empty
+  prompt) or ``synthetic_prompts`` {"n", "length", "seed"}.  ``timing`` is optional and
   measured on the GPU when absent (metrics.measured_params).
 
 Run-level extensions: ``adaptive_gamma``, ``gamma_max`` and ``batch`` (B
@@ -283,8 +284,8 @@ def load_prompts(cfg: RunConfig, vocab: Optional[int] = None) -> List[List[int]]
             ids = [int(x) for x in line.split()]
         except ValueError as exc:
             raise ConfigError("$.prompts", f"line {i + 1}: token ids must be integers ({exc})") from exc
-        if not ids or (vocab is not None and any(not 0 <= t < vocab for t in ids)):
-            raise ConfigError("$.prompts", f"line {i + 1}: needs 1+ token ids in [0, {vocab})")
+        if vocab is not None and any(not 0 <= t < vocab for t in ids):
+            raise ConfigError("$.prompts", f"line {i + 1}: token ids must be in [0, {vocab})")
         out.append(ids)
     return out
 
@@ -346,7 +347,7 @@ def run(cfg: RunConfig, out_dir: Optional[str] = None, real_latency: bool = Fals
     if models is None:
         max_seq = 1024
         if isinstance(cfg.model, TransformerSpec):
-            longest = max(len(p) for p in load_prompts(cfg))
+            longest = max(len(p) for p in load_prompts(cfg)) + 1  # + BOS
             max_seq = longest + cfg.max_new_tokens + 2 * max(cfg.gamma or 1, cfg.gamma_max) + 16
         models = build_models(cfg, max_seq=max_seq)
     draft, target, eos_id, timing = models

@@ -171,12 +171,12 @@ def test_transformer_checkpoint_run(tmp_path):
         (tmp_path / name / "config.json").write_text(json.dumps(
             {"num_hidden_layers": layers, "hidden_size": d, "num_attention_heads": 4, "num_key_value_heads": 2,
              "intermediate_size": F, "vocab_size": V}))
-    (tmp_path / "p.txt").write_text("5 17 300 9\n900 31 2\n")
+    (tmp_path / "p.txt").write_text("5 17 300 9\n\n900 31 2\n")  # the empty line decodes from BOS
     doc = {"engine": "pearl", "gamma": 3, "max_new_tokens": 20, "seed": 4, "prompts": str(tmp_path / "p.txt"),
            "model": {"transformer": {"checkpoint": {"target": str(tmp_path / "target"),
                                                     "draft": str(tmp_path / "draft")}}}}
     (tmp_path / "cfg.json").write_text(json.dumps(doc))
     assert runconfig.main(["run", "--config", str(tmp_path / "cfg.json"), "--out", str(tmp_path / "o")]) == 0
     out = (tmp_path / "o" / "outputs.txt").read_text().splitlines()
-    assert len(out) == 2 and all(len(line.split()) == 20 for line in out)
+    assert len(out) == 3 and all(len(line.split()) == 20 for line in out)
     assert all(0 <= int(x) < V for line in out for x in line.split())
