@@ -206,9 +206,6 @@ int pearl_llama_destroy(void* handle);
 /* Forward flags */
 #define PEARL_FWD_ADVANCE 1     /* *pos += n_tokens when done              */
 #define PEARL_FWD_LAST_LOGITS 2 /* logits only for the last token ([1, V]) */
-#define PEARL_FWD_PERSISTENT 4  /* tcgen05 models, windows <= 16 tokens:  \
-                                   run as one persistent kernel (same bits \
-                                   as the default one-kernel-per-op path)  */
 
 /* Run n_tokens tokens (device int32[n_tokens]) at positions *pos .. *pos+n-1
  * (pos is a device int32 so graph replays see its current value), append
@@ -250,20 +247,13 @@ int pearl_green_streams(int first_sms, void** first_stream, void** rest_stream, 
 
 /* Diagnostic: copy an internal activation buffer of the last forward
  * (0 residual h fp32 [T, d]; 1 x, 2 q, 3 o, 4 act bf16; 5 stream-K tile
- * flags int32; 6 the persistent kernel's phase counters) to device dst.  With
+ * flags int32; 6 folded-norm per-tile sums of h^2 fp32 [ceil(d/128), T])
+ * to device dst.  With
  * PEARL_STOP=k in the environment a forward runs only its first k ops. */
 int pearl_llama_debug_buffer(void* handle, int which, void* dst, size_t bytes, void* stream);
 
-/* Diagnostic: one forward through the persistent kernel (tcgen05 models,
- * n_tokens <= 16) with per-CTA phase timestamps.  out[3p + 0] = phase kind
- * (0 embed, 1 rmsnorm, 2 GEMM, 3 attention), out[3p + 1] / out[3p + 2] = us
- * from the first CTA start until the last / first CTA finished phase p.
- * Returns the number of phases (or a negative error). */
-int pearl_llama_mega_trace(void* handle, const int32_t* tokens, int n_tokens, int32_t* pos, int flags,
-                           float* logits, float* out, int max_phases, void* stream);
-
 /* Diagnostic: one eager forward with an event after every launch; out_ms
- * (float[10]) receives device ms per op {embed, rmsnorm, qkv, attention, o,
+ * (float[10]) receives device ms per op {embed, (unused), qkv, attention, o,
  * gate_up, down, lm_head, other} and the total. */
 int pearl_llama_profile(void* handle, const int32_t* tokens, int n_tokens, int32_t* pos, float* logits,
                         float* out_ms, void* stream);

@@ -12,7 +12,14 @@ plain PyTorch restatement of the architecture the B200 kernels implement
 ``bf16_points=True`` rounds at exactly the points the kernels store bf16
 (activations fed to GEMMs, q/k/v, attention output), so only fp32
 accumulation order differs from the GPU; ``bf16_points=False`` is the pure
-fp32 math.  ``OracleLlama`` adds a KV cache and an LCP-reusing ``next_dist``
+fp32 math.  ``norm_fold`` selects where RMSNorm's two factors meet the
+bf16 rounding, as in the two GEMM engines (paper_2408_11850_b200/csrc/llama.cu):
+
+  norm_fold=False (CUDA-core K2):  y = W . bf16(h * rs * g)
+  norm_fold=True  (tcgen05 K3):    y = rs * (W . bf16(h * g))
+
+with rs = 1 / sqrt(mean(h^2) + eps); the two are the same real-number
+function of h (and identical when bf16_points=False).  ``OracleLlama`` adds a KV cache and an LCP-reusing ``next_dist``
 so the oracle engine (oracle/engine.py) can drive it as the CPU baseline.
 """
 
@@ -45,8 +52,9 @@ class OracleLlama:
     """
 
     def __init__(self, cfg, weights: Dict, device="cpu", bf16_points: bool = True, max_seq: int = 1024,
-                 mm_dtype=torch.float32, bos_id: int = 1, temperature: float = 1.0):
+                 mm_dtype=torch.float32, bos_id: int = 1, temperature: float = 1.0, norm_fold: bool = False):
         self.cfg = cfg
+        self.fold = norm_fold
         self.dev = torch.device(device)
         self.b = bf16_points
         self.mm = mm_dtype
@@ -69,11 +77,16 @@ class OracleLlama:
         self.cached: List[int] = []
 
     def _norm(self, h, g):
+        """(GEMM operand, per-row scale applied to the GEMM output)."""
         ms = (h * h).mean(dim=-1, keepdim=True)
-        return _bf(h * torch.rsqrt(ms + self.cfg.norm_eps) * g, self.b)
+        rs = torch.rsqrt(ms + self.cfg.norm_eps)
+        if self.fold:
+            return _bf(h * g, self.b), rs
+        return _bf(h * rs * g, self.b), None
 
-    def _mm(self, x, w):
-        return (x.to(self.mm) @ w.T).float()
+    def _mm(self, x, w, scale=None):
+        y = (x.to(self.mm) @ w.T).float()
+        return y if scale is None else y * scale
 
     def _rope(self, x, pos):  # x [M, heads, hd]
         c = self.cos[pos][:, None, :]
@@ -93,8 +106,8 @@ class OracleLlama:
         pos = torch.arange(start, start + M, device=self.dev)
         h = self.embed[torch.tensor(list(tokens), device=self.dev)].float()
         for l, Lw in enumerate(self.layers):
-            x = self._norm(h, Lw["attn_norm"])
-            qkv = self._mm(x, Lw["wqkv"])
+            x, rs = self._norm(h, Lw["attn_norm"])
+            qkv = self._mm(x, Lw["wqkv"], rs)
             q = qkv[:, :H * hd].view(M, H, hd)
             k = qkv[:, H * hd:(H + KV) * hd].view(M, KV, hd)
             v = qkv[:, (H + KV) * hd:].view(M, KV, hd)
@@ -115,13 +128,13 @@ class OracleLlama:
             p = torch.softmax(s, dim=-1)
             o = _bf(torch.einsum("hmc,chd->mhd", p, Vv).reshape(M, H * hd), self.b)
             h = h + self._mm(o, Lw["wo"])
-            x = self._norm(h, Lw["mlp_norm"])
-            gu = self._mm(x, Lw["w_gate_up"])
+            x, rs = self._norm(h, Lw["mlp_norm"])
+            gu = self._mm(x, Lw["w_gate_up"], rs)
             g, u = gu[:, 0::2], gu[:, 1::2]
             a = _bf(g / (1.0 + torch.exp(-g)) * u, self.b)
             h = h + self._mm(a, Lw["w_down"])
-        x = self._norm(h, self.final_norm)
-        return self._mm(x, self.lm_head)
+        x, rs = self._norm(h, self.final_norm)
+        return self._mm(x, self.lm_head, rs)
 
     # -- SequenceModel-style adapter for the oracle engine --------------------
     def next_dist(self, prefix: Sequence[int]):

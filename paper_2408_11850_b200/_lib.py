@@ -68,7 +68,6 @@ SIGNATURES = {
     "pearl_llama_profile": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp, _vp]),
     "pearl_llama_set_l2_window": (_i32, [_vp, _vp, ctypes.c_size_t, _vp]),
     "pearl_green_streams": (_i32, [_i32, _vp, _vp, _vp, _vp]),
-    "pearl_llama_mega_trace": (_i32, [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _vp]),
     "pearl_llama_debug_buffer": (_i32, [_vp, _i32, _vp, ctypes.c_size_t, _vp]),
     "pearl_gemm": (_i32, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
     "pearl_gemm_splits": (_i32, [_i32, _i32]),

@@ -38,7 +38,42 @@ struct EpiArgs {
   int32_t* adv_pos; // optional: one thread adds adv_n to *adv_pos once the kernel's
   int adv_n;        //   inputs are ready (folds the forward's position advance into
                     //   its last GEMM: every earlier reader of pos has completed)
+  // RMSNorm folded into the tcgen05 GEMMs (no norm kernel; see llama.cu):
+  //  * producer side (RESID): also write the next GEMM's operand
+  //    x_out[t] = bf16(h[t] * gain) and, per 128-row tile, the tile's sum of
+  //    h^2 into ss_out[tile * ss_ld + t];
+  //  * consumer side (QKV / SWIGLU / STORE_F32): scale every output by
+  //    rs[t] = 1 / sqrt(sum_tiles ss_in[tile * ss_ld + t] / d + eps), computed
+  //    once per CTA (norm_rs) and passed to epilogue_tile.
+  bf16* x_out;
+  const float* gain;
+  float* ss_out;
+  const float* ss_in;
+  int ss_ld;        // tokens per ss row (the model's max_tokens)
+  int ss_tiles;     // tiles summed by the consumer (ceil(d / 128))
+  int norm_d;
+  float norm_eps;
 };
+
+// Sum of squares of four consecutive h values, reduced over a warp's 32
+// lanes (= the 32 four-row groups of one 128-row tile) in a fixed xor tree.
+// The embedding kernel and the residual epilogue use exactly this order.
+__device__ __forceinline__ float tile_sumsq(float4 h) {
+  float s = h.x * h.x;
+  s = fmaf(h.y, h.y, s);
+  s = fmaf(h.z, h.z, s);
+  s = fmaf(h.w, h.w, s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// rs[t] of token t from the producer's per-tile partial sums (fixed order).
+__device__ __forceinline__ float norm_rs(const EpiArgs& e, int t) {
+  float tot = 0.f;
+  for (int k = 0; k < e.ss_tiles; ++k) tot += __ldcg(e.ss_in + static_cast<size_t>(k) * e.ss_ld + t);
+  return 1.0f / sqrtf(tot / static_cast<float>(e.norm_d) + e.norm_eps);
+}
 
 // The per-element arithmetic, with explicit rounding (no FMA contraction), so
 // every call site -- GEMV, per-GEMM tcgen05 kernel, persistent forward --
@@ -122,9 +157,14 @@ __device__ __forceinline__ float4 epi_rows4(const float* E, int ES, int g, int t
   return make_float4(E[(g * 4) * ES + t], E[(g * 4 + 1) * ES + t], E[(g * 4 + 2) * ES + t], E[(g * 4 + 3) * ES + t]);
 }
 
+__device__ __forceinline__ float4 scale4(float4 v, float r) {
+  return make_float4(__fmul_rn(v.x, r), __fmul_rn(v.y, r), __fmul_rn(v.z, r), __fmul_rn(v.w, r));
+}
+
+// rs: per-token norm scales in smem (nullptr: no folded norm).
 template <int MAXI, bool TR = false>
 __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const float* E, int ES, int M, int N,
-                                              int et) {
+                                              int et, const float* rs = nullptr) {
   constexpr int kGroups = 32;  // 128 rows / 4
   const int nitems = kGroups * M;
   switch (e.kind) {
@@ -134,7 +174,8 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
         float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
-        const float4 v = epi_rows4<TR>(E, ES, g, t);
+        float4 v = epi_rows4<TR>(E, ES, g, t);
+        if (rs) v = scale4(v, rs[t]);
         if (n0 + 3 < N && (e.ld & 3) == 0) {
           *reinterpret_cast<float4*>(o) = v;
         } else {
@@ -155,15 +196,30 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
-        if (idx >= nitems || n0 >= N) continue;
-        float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
-        const float4 v = epi_rows4<TR>(E, ES, g, t);
-        if (n0 + 3 < N) {
-          *reinterpret_cast<float4*>(o) = make_float4(hv[i].x + v.x, hv[i].y + v.y, hv[i].z + v.z, hv[i].w + v.w);
-        } else {
-          const float w[4] = {v.x, v.y, v.z, v.w};
-          for (int r = 0; r < 4; ++r)
-            if (n0 + r < N) o[r] += w[r];
+        if (idx >= nitems) continue;  // uniform per warp: a warp's 32 lanes are one token's 32 groups
+        float4 hn = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (n0 < N) {
+          float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
+          const float4 v = epi_rows4<TR>(E, ES, g, t);
+          if (n0 + 3 < N) {
+            hn = make_float4(hv[i].x + v.x, hv[i].y + v.y, hv[i].z + v.z, hv[i].w + v.w);
+            *reinterpret_cast<float4*>(o) = hn;
+          } else {
+            const float w[4] = {v.x, v.y, v.z, v.w};
+            for (int r = 0; r < 4; ++r)
+              if (n0 + r < N) o[r] += w[r];
+          }
+        }
+        if (e.x_out) {
+          if (n0 + 3 < N) {
+            const float4 gv = __ldg(reinterpret_cast<const float4*>(e.gain + n0));  // same for every token: cached
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(hn.x * gv.x, hn.y * gv.y);
+            const __nv_bfloat162 hi = __floats2bfloat162_rn(hn.z * gv.z, hn.w * gv.w);
+            *reinterpret_cast<uint2*>(e.x_out + static_cast<size_t>(t) * e.ld + n0) =
+                make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+          }
+          const float ss = tile_sumsq(hn);
+          if (g == 0) e.ss_out[static_cast<size_t>(tile) * e.ss_ld + t] = ss;
         }
       }
       break;
@@ -173,7 +229,8 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
-        const float4 v = epi_rows4<TR>(E, ES, g, t);
+        float4 v = epi_rows4<TR>(E, ES, g, t);
+        if (rs) v = scale4(v, rs[t]);
         e.out_bf16[static_cast<size_t>(t) * e.ld + n0 / 2] = __float2bfloat16(swiglu1(v.x, v.y));
         e.out_bf16[static_cast<size_t>(t) * e.ld + (n0 + 2) / 2] = __float2bfloat16(swiglu1(v.z, v.w));
       }
@@ -197,7 +254,8 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
         if (idx >= nitems || n0 >= N) continue;
         const int p = e.tok_pos ? e.tok_pos[t] : p0 + t;
         const size_t so = epi_slot_off(e, t);
-        const float4 v4 = epi_rows4<TR>(E, ES, g, t);
+        float4 v4 = epi_rows4<TR>(E, ES, g, t);
+        if (rs) v4 = scale4(v4, rs[t]);
         const float v[4] = {v4.x, v4.y, v4.z, v4.w};
         if (n0 < e.n_q + e.n_kv) {
           float w[4];

@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
   constexpr int stages = C::kStages;
   constexpr int ES = C::kEStride;
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+  __shared__ float s_rs[kMaxTokTiles * kTokTile];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   float* E = reinterpret_cast<float*>(smem + stages * stage_bytes);
@@ -167,6 +168,15 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
     const int row = lanegrp * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127
     const int Mp = (a.M + 3) & ~3;  // partial row stride (float4 aligned)
+    // folded RMSNorm: the per-token scales, once per CTA, while the first
+    // accumulator is still being filled
+    const float* rsp = nullptr;
+    if (a.e.ss_in != nullptr) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int t = et; t < a.M; t += kEpiThreads) s_rs[t] = norm_rs(a.e, t);
+      epi_bar();
+      rsp = s_rs;
+    }
     int ui = 0;
     for (long long x = r0; x < r1; ++ui) {
       const Unit u = unit_at(a, x, r1);
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         if (et == 0) a.flags[tile] = 0;
       }
       epi_bar();
-      epilogue_tile<NT * 4, true>(a.e, tile, E, ES, a.M, a.N, et);
+      epilogue_tile<NT * 4, true>(a.e, tile, E, ES, a.M, a.N, et, rsp);
       epi_bar();
     }
   }
@@ -326,7 +336,7 @@ int tc_seg_max(int tiles, int KB, int G) {
 
 int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   if (c.max_tokens > kMaxTokTiles * kTokTile) {
-    set_error("tcgen05 path supports max_tokens <= 64");
+    set_error("tcgen05 path supports max_tokens <= 128");
     return PEARL_ERR_ARG;
   }
   int dev = 0;

@@ -1,7 +1,7 @@
 // Shared device building blocks of the tcgen05 contraction kernels (K3):
 // tile constants, PTX wrappers for mbarrier / TMA / tcgen05, the K-major
 // SWIZZLE_128B UMMA descriptor, and the stream-K unit walker.  Used by the
-// per-GEMM kernel (gemm_tc.cu) and the persistent forward kernel (fwd_mega.cu).
+// tcgen05 GEMM kernel (gemm_tc.cu).
 #pragma once
 
 #include <cuda.h>

@@ -179,11 +179,22 @@ def init_weights(cfg: LlamaConfig, align: AlignSpec, model_seed: int, device,
     return w
 
 
-def init_pair(pair: str, align: AlignSpec = AlignSpec(), device=None):
-    """(target_weights, draft_weights, target_cfg, draft_cfg) for a named pair."""
-    device = device or _device.require_cuda()
+def pair_configs(pair: str, depth: Optional[tuple] = None) -> tuple:
+    """(target_cfg, draft_cfg) of a named pair; ``depth=(Lt, Ld)`` keeps every
+    width (d, heads, KV heads, FFN, vocab, rope theta) and only cuts the layer
+    count -- the reduced-depth, full-width parity configs."""
     tname, dname = PAIRS[pair]
     tc, dc = PRESETS[tname], PRESETS[dname]
+    if depth is not None:
+        tc = replace(tc, name=f"{tc.name}-L{depth[0]}", n_layers=int(depth[0]))
+        dc = replace(dc, name=f"{dc.name}-L{depth[1]}", n_layers=int(depth[1]))
+    return tc, dc
+
+
+def init_pair(pair: str, align: AlignSpec = AlignSpec(), device=None, depth: Optional[tuple] = None):
+    """(target_weights, draft_weights, target_cfg, draft_cfg) for a named pair."""
+    device = device or _device.require_cuda()
+    tc, dc = pair_configs(pair, depth)
     assert tc.vocab == dc.vocab
     shared = _shared_tables(tc.vocab, align, device)
     tw = init_weights(tc, align, align.seed + 1, device, shared)
@@ -390,7 +401,7 @@ def inv_temp(t: float) -> float:
 def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: str = "auto",
                align: AlignSpec = AlignSpec(), max_seq: int = 1024, max_tokens: int = 64,
                temperature: float = 1.0, l2_draft: Optional[bool] = None, draft_sms: Optional[int] = None,
-               n_slots: int = 1):
+               n_slots: int = 1, depth: Optional[tuple] = None):
     """(target LlamaModel, draft LlamaModel) with controlled-alignment random weights.
 
     ``l2_draft``: keep the draft's streamed weights in persisting L2
@@ -402,7 +413,8 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
     GEMV (K2) for drafts under 1 GB of weights, where a forward is
     launch-latency bound and K2 is as fast; tcgen05 (K3) for larger drafts,
     where it streams faster (tools/draft_times.py: 1.3B 1.21 vs 1.50 ms,
-    8B 3.41 vs 4.51 ms per token on B200)."""
+    8B 3.41 vs 4.51 ms per token on B200).  ``depth=(Lt, Ld)``: reduced-depth,
+    full-width variant of the pair (parity tests at the BASELINE shapes)."""
     if l2_draft is None:
         l2_draft = os.environ.get("PEARL_L2_DRAFT", "0") == "1"
     if draft_sms is None:
@@ -428,7 +440,7 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
             import warnings
             warnings.warn(f"green-context partition unavailable ({_lib.load().pearl_last_error().decode()}); "
                           "draft and target share all SMs")
-    tw, dw, tc, dc = init_pair(pair, align)
+    tw, dw, tc, dc = init_pair(pair, align, depth=depth)
     target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq,
                         max_tokens=max_tokens if gemm_target == "tcgen05" else min(max_tokens, 64),
                         temperature=temperature, sm_count=target_sms, n_slots=n_slots)

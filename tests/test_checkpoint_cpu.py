@@ -144,5 +144,5 @@ def test_hf_checkpoint_runs_on_the_kernels(tmp_path, gemm):
     m = llama.LlamaModel(cfg, w, gemm=gemm, max_seq=64, max_tokens=32)
     toks = [1, 5, 900, 17, 4, 4, 300, 12, 1000, 2]
     got = m.forward_logits(toks).cpu()
-    want = OracleLlama(cfg, w, device="cuda", bf16_points=True, max_seq=64).forward(toks, 0).cpu()
+    want = OracleLlama(cfg, w, device="cuda", bf16_points=True, max_seq=64, norm_fold=gemm == "tcgen05").forward(toks, 0).cpu()
     assert ((got - want).abs() <= 5e-2 + 1e-2 * want.abs()).all()
