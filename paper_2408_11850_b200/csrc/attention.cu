@@ -98,23 +98,55 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
   const int n = lane >> 2, q = lane & 3;
   const int crank = static_cast<int>(cluster.block_rank());
   const int CS = static_cast<int>(cluster.num_blocks());  // CTAs per (row block, KV head)
-  const int cid = blockIdx.x / CS;
-  const int b = cid / a.KV, kvh = cid % a.KV;
   const int g = a.H / a.KV;
-  const int R_all = g * a.M;
-  const int r0 = b * a.rb, r1 = min(r0 + a.rb, R_all), R = r1 - r0;
-  // Sequence mode: positions < p0 hold K/V of earlier forwards (complete:
-  // the forward's embedding kernel waited for them), so they may be read
-  // before griddepcontrol.wait; slot mode reads everything after it.
+  const int tpb = a.tpb;  // tokens per row block (tpb * g <= 16 rows)
   const bool seq_mode = a.tok_pos == nullptr;
-  if (!seq_mode) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Row blocks: runs of consecutive tokens sharing a KV slot (sequence mode:
+  // one run), cut into chunks of tpb tokens.  Every CTA derives the same
+  // table; tok_slot / tok_pos / *pos were written before this forward began
+  // (its embedding kernel waited for them), so this runs before the wait.
+  __shared__ int s_bstart[kAttnMaxTok + 1];
+  __shared__ int s_nblk;
+  if (seq_mode) {
+    if (threadIdx.x == 0) s_nblk = (a.M + tpb - 1) / tpb;
+  } else if (warp == 0) {
+    int nb = 0, rs = 0, prev = -1;
+    for (int c0 = 0; c0 < a.M; c0 += 32) {
+      const int t = c0 + lane;
+      const int sl = t < a.M ? a.tok_slot[t] : -2;
+      int up = __shfl_up_sync(0xffffffffu, sl, 1);
+      if (lane == 0) up = prev;
+      const bool run0 = t < a.M && (t == 0 || sl != up);
+      const unsigned rm = __ballot_sync(0xffffffffu, run0) & (0xffffffffu >> (31 - lane));
+      const int my_rs = rm ? c0 + 31 - __clz(rm) : rs;  // this token's run start
+      const bool bs = t < a.M && (t - my_rs) % tpb == 0;
+      const unsigned bm = __ballot_sync(0xffffffffu, bs);
+      if (bs) s_bstart[nb + __popc(bm & ((1u << lane) - 1))] = t;
+      nb += __popc(bm);
+      rs = __shfl_sync(0xffffffffu, my_rs, 31);
+      prev = __shfl_sync(0xffffffffu, sl, 31);
+    }
+    if (lane == 0) {
+      s_nblk = nb;
+      s_bstart[nb] = a.M;
+    }
+  }
+  __syncthreads();
+  const int nblk = s_nblk;
   const int p0 = seq_mode ? *a.pos + a.pos_add : 0;
-  const int pmax = tok_position(a, p0, (r1 - 1) / g);
   const size_t kvs = static_cast<size_t>(a.KV) * HD;  // elements per cache position
-  const size_t so = a.tok_slot ? static_cast<size_t>(a.tok_slot[r0 / g]) * static_cast<size_t>(a.slot_stride) : 0;
+  const int nclus = gridDim.x / CS;
+  bool first = true;
+  for (int item = blockIdx.x / CS; item < nblk * a.KV; item += nclus) {
+  const int b = item / a.KV, kvh = item % a.KV;
+  const int t0 = seq_mode ? b * tpb : s_bstart[b];
+  const int t1 = seq_mode ? min(t0 + tpb, a.M) : s_bstart[b + 1];
+  const int r0 = t0 * g, r1 = t1 * g, R = r1 - r0;
+  const int pmax = tok_position(a, p0, t1 - 1);
+  const size_t so = a.tok_slot ? static_cast<size_t>(a.tok_slot[t0]) * static_cast<size_t>(a.slot_stride) : 0;
   const bf16* kc = a.kc + so + static_cast<size_t>(kvh) * HD;
   const bf16* vc = a.vc + so + static_cast<size_t>(kvh) * HD;
-  // segment js of this warp: 32 positions at 32 (js * 32 + 4 crank + warp)
+  // segment js of this warp: 32 positions at 32 ((js CS + crank) 4 + warp)
   auto seg_p0 = [&](int js) { return 32 * ((js * CS + crank) * kWarps + warp); };
 
   uint4 kb[4][J], vb[4][J];
@@ -122,8 +154,8 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < J; ++j) kb[i][j] = vb[i][j] = make_uint4(0, 0, 0, 0);
-  const int old_hi = seq_mode ? min(p0, pmax + 1) - 1 : -1;  // last position loadable before the wait
-  if (seq_mode) {
+  const int old_hi = (seq_mode && first) ? min(p0, pmax + 1) - 1 : -1;  // last position loadable before the wait
+  if (first) {
     if (seg_p0(0) <= pmax) load_kv<HD>(kc, vc, kvs, seg_p0(0), lane, 0, old_hi, kb, vb);
     // later segments' old positions: warm L2 while the QKV GEMM drains
     for (int js = 1; js < a.spw; ++js) {
@@ -139,8 +171,8 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
       }
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // query rows lo = n, hi = n + 8 of the 16-row tile (rows >= R are zero)
   uint4 qa[2][J];
@@ -309,6 +341,13 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
     a.o[(static_cast<size_t>(t) * a.H + h) * HD + d] = __float2bfloat16(O / cw[kAttnMaxRb * kAttnCluster + rr]);
   }
   if (CS > 1) cluster.sync();  // the peers' states stay alive until every CTA has read them
+  else __syncthreads();         // smem reuse by the next item
+  first = false;
+  }
+  if (first) {  // no work for this cluster: still order after the producer
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
 }
 
 std::once_flag g_once;
@@ -334,7 +373,10 @@ int attn_init() {
   return PEARL_OK;
 }
 
-int attn_cluster_size() {
+int attn_cluster_size(bool slot_mode) {
+  // slot mode (batched sequences): many short token runs, one item each --
+  // single-CTA clusters keep every item's latency chain short
+  if (slot_mode) return 1;
   static const int cs = [] {
     const char* v = std::getenv("PEARL_ATTN_CLUSTER");
     const int x = v ? std::atoi(v) : kAttnClusterDefault;
@@ -351,19 +393,19 @@ static int attn_minb() {
   return m;
 }
 
-void attn_plan(const AttnShape& s, int* rb, int* nrb, int* spw, int* grid) {
+void attn_plan(const AttnShape& s, int* tpb, int* spw, int* grid) {
   const int g = s.H / s.KV;
-  const int R = g * s.M;
-  // one 16-row MMA tile per cluster; slot mode keeps a block inside one
-  // token (its own cache slot): the token's g query heads
-  const int r = s.slot_mode ? g : std::min(kAttnMaxRb, R);
-  *rb = r;
-  *nrb = (R + r - 1) / r;
+  // tokens per row block: one 16-row MMA tile of (token, query head) rows
+  *tpb = std::max(1, kAttnMaxRb / g);
   // segments per warp: the cluster's CS CTAs x 4 warps cover the whole
   // cache in spw rounds of 128 CS positions (a function of max_seq only)
-  const int CS = attn_cluster_size();
+  const int CS = attn_cluster_size(s.slot_mode);
   *spw = (s.max_seq + 128 * CS - 1) / (128 * CS);
-  *grid = *nrb * s.KV * CS;
+  // row blocks: sequence mode ceil(M / tpb); slot mode at most one per token
+  // run chunk, bounded by M.  One cluster per (block, KV head) item: items
+  // past the device-side block count exit at once
+  const int nblk_max = s.slot_mode ? s.M : (s.M + *tpb - 1) / *tpb;
+  *grid = nblk_max * s.KV * CS;
 }
 
 int attn_launch(const AttnArgs& a, int hd, int grid, cudaStream_t st) {
@@ -373,7 +415,7 @@ int attn_launch(const AttnArgs& a, int hd, int grid, cudaStream_t st) {
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = attn_cluster_size();
+  at[0].val.clusterDim.x = attn_cluster_size(a.tok_pos != nullptr);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -41,6 +41,7 @@ constexpr int kAttnThreads = 128;   // 4 warps
 constexpr int kAttnCluster = 8;     // largest cluster (CTAs per (row block, KV head))
 constexpr int kAttnClusterDefault = 4;  // measured best on B200 (7B M=4: 1 -> 3.09, 2 -> 2.98, 4 -> 2.97 ms)
 constexpr int kAttnMaxRb = 16;      // rows per block (one m16n8k16 row tile)
+constexpr int kAttnMaxTok = 128;    // tokens per launch (a model's max_tokens)
 
 struct AttnArgs {
   const __nv_bfloat16* q;   // [M, H, hd] (post-RoPE)
@@ -54,10 +55,9 @@ struct AttnArgs {
   long long slot_stride;    // elements per slot
   int M, H, KV;
   float scale;
-  int rb;                   // rows per row block (sequence mode: consecutive rows
-                            // t * g + j; slot mode: rb = g, one token per block)
-  int nrb;                  // row blocks
-  int spw;                  // segments per warp (rounds of 1024 positions)
+  int tpb;                  // tokens per row block (rows t * g + j, <= 16); slot mode
+                            // blocks never straddle a run of same-slot tokens
+  int spw;                  // segments per warp (rounds of 128 x cluster-size positions)
 };
 
 // Host: plan (rb, nrb) for a window of M tokens, launch on stream st.
@@ -65,8 +65,8 @@ struct AttnShape {
   int M, H, KV, hd, max_seq, num_sms;
   bool slot_mode;
 };
-void attn_plan(const AttnShape& s, int* rb, int* nrb, int* spw, int* grid);
-int attn_cluster_size();  // CTAs per cluster (PEARL_ATTN_CLUSTER: 1, 2, 4, 8)
+void attn_plan(const AttnShape& s, int* tpb, int* spw, int* grid);
+int attn_cluster_size(bool slot_mode);  // CTAs per cluster (PEARL_ATTN_CLUSTER: 1, 2, 4, 8)
 int attn_launch(const AttnArgs& a, int hd, int grid, cudaStream_t st);
 int attn_init();  // one-time kernel attributes
 

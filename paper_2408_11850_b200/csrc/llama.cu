@@ -454,8 +454,8 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   if (halt()) return PEARL_OK;
   const size_t slot_kv = static_cast<size_t>(c.max_seq) * nkv;
   const size_t layer_kv = static_cast<size_t>(std::max(1, c.n_slots)) * slot_kv;
-  int rb = 1, nrb = 1, spw = 1, agrid = 1;
-  attn_plan(AttnShape{M, H, KV, hd, c.max_seq, m.num_sms, tok_pos != nullptr}, &rb, &nrb, &spw, &agrid);
+  int tpb = 1, spw = 1, agrid = 1;
+  attn_plan(AttnShape{M, H, KV, hd, c.max_seq, m.num_sms, tok_pos != nullptr}, &tpb, &spw, &agrid);
   for (int l = 0; l < L; ++l) {
     const LayerW& Lw = m.layers[l];
     EpiArgs e{};
@@ -494,8 +494,7 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
       aa.H = H;
       aa.KV = KV;
       aa.scale = 1.0f / sqrtf(static_cast<float>(hd));
-      aa.rb = rb;
-      aa.nrb = nrb;
+      aa.tpb = tpb;
       aa.spw = spw;
       rc = attn_launch(aa, hd, agrid, st);
       if (rc) return rc;

@@ -25,8 +25,8 @@ from __future__ import annotations
 import ctypes
 import math
 import os
-from dataclasses import replace
-from typing import Dict, List, Optional, Sequence
+from dataclasses import dataclass, replace
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -339,6 +339,82 @@ def pearl_tokens_per_step(alpha: float, gamma: int) -> float:
     return (1.0 - ag) / ((1.0 - a) * (1.0 - ag + a))
 
 
+@dataclass
+class PlannerCalibration:
+    """Frozen step-time model of one (draft, target) pair on one device.
+
+    ``step_s[(pre_verify, gamma)]`` = device seconds of that PEARL step graph
+    (draft catch-up m0 = 1), measured once by :func:`calibrate_planner`;
+    ``alpha0`` = the pair's acceptance, the prior every decode starts from.
+    With a calibration installed (:func:`set_planner_calibration`) the
+    adaptive planner prices draft lengths from this table only -- no timing
+    measured during a decode feeds back -- so a decode's gamma schedule is a
+    function of its tokens alone and identical on every box that loads the
+    same table."""
+
+    step_s: Dict[Tuple[bool, int], float]
+    alpha0: float = 0.75
+    source: str = "live"
+
+    def to_json(self) -> dict:
+        return {"step_ms": {f"{'pre' if p else 'post'}:{g}": round(v * 1e3, 5) for (p, g), v in
+                            sorted(self.step_s.items())},
+                "alpha0": round(self.alpha0, 4), "source": self.source}
+
+    @classmethod
+    def from_json(cls, d: dict, source: str = "file") -> "PlannerCalibration":
+        st = {}
+        for k, v in d["step_ms"].items():
+            mode, g = k.split(":")
+            st[(mode == "pre", int(g))] = float(v) / 1e3
+        return cls(st, float(d.get("alpha0", 0.75)), source)
+
+
+def _frozen_key(draft) -> str:
+    return "_pearl_frozen_" + str(id(draft))
+
+
+def set_planner_calibration(draft, target, cal: Optional[PlannerCalibration]) -> None:
+    """Install (or, with None, remove) a frozen planner calibration for a pair."""
+    if cal is None:
+        target.__dict__.pop(_frozen_key(draft), None)
+    else:
+        target.__dict__[_frozen_key(draft)] = cal
+
+
+def calibrate_planner(draft, target, prefix: Sequence[int], gamma_max: int, temperature: float = 1.0,
+                      greedy: bool = False, new_tokens: int = 96, seed: int = 12345,
+                      concurrent: bool = True) -> PlannerCalibration:
+    """Measure the step-time table: one fixed-gamma decode per grid gamma
+    (both step kinds occur), median device time per (kind, gamma)."""
+    from .engines import EngineConfig, empirical_acceptance
+    prev = target.__dict__.pop(_frozen_key(draft), None)
+    times: Dict[Tuple[bool, int], List[float]] = {}
+    steps_all = []
+    try:
+        for g in [g for g in _GammaPlanner.GRID if g <= gamma_max]:
+            cfg = EngineConfig(gamma=g, max_new_tokens=new_tokens, seed=seed, greedy=greedy,
+                               temperature=temperature, gamma_max=max(gamma_max, g))
+            for rep in range(2):  # the first decode captures the graphs
+                res = decode_pearl(draft, target, prefix, cfg, concurrent=concurrent)
+            for pre, gg, m0, t in res.stats["step_log"]:
+                if m0 == 1:
+                    times.setdefault((pre, gg), []).append(t)
+            steps_all += list(res.steps)
+    finally:
+        if prev is not None:
+            target.__dict__[_frozen_key(draft)] = prev
+    step_s = {k: float(np.median(v)) for k, v in times.items()}
+    # a kind never reached at some gamma (e.g. post-verify at alpha ~ 0): the
+    # other kind's time, the closest proxy
+    for g in [g for g in _GammaPlanner.GRID if g <= gamma_max]:
+        for pre in (True, False):
+            if (pre, g) not in step_s and (not pre, g) in step_s:
+                step_s[(pre, g)] = step_s[(not pre, g)]
+    alpha = empirical_acceptance(steps_all)
+    return PlannerCalibration(step_s, float(alpha) if alpha is not None else 0.75, "live")
+
+
 class _GammaPlanner:
     """Adaptive draft length (paper §3.4): gamma maximising expected PEARL
     tokens per unit of device time,
@@ -358,6 +434,17 @@ class _GammaPlanner:
     GRID = (1, 2, 3, 4, 6, 8, 12, 16, 20, 24, 32, 48, 64)
 
     def __init__(self, target: LlamaModel, draft: LlamaModel, gamma_max: int, gamma0: int):
+        frozen = target.__dict__.get(_frozen_key(draft))
+        self.frozen = frozen is not None
+        if self.frozen:
+            # frozen table: no calibration forwards, no feedback from decode timings
+            self.meas = dict(frozen.step_s)
+            self.t_d, self.t_t = 0.0, {1: 1.0}
+            self.gmax = gamma_max
+            self.acc, self.exam = 8.0 * frozen.alpha0, 8.0
+            self.gamma = gamma0
+            self.started = False
+            return
         key = "_pearl_calib_" + str(id(draft))
         cal = target.__dict__.get(key)
         if cal is None:
@@ -395,13 +482,15 @@ class _GammaPlanner:
     def observe(self, accepted: int, rejected: int) -> None:
         self.acc += accepted
         self.exam += accepted + rejected
-        if hasattr(self, "pair"):
+        if hasattr(self, "pair") and not self.frozen:
             self.pair[0] += accepted
             self.pair[1] += accepted + rejected
 
     def observe_time(self, pre: bool, g: int, seconds: float) -> None:
         """Measured device time of one step graph (co-resident path only: the
         split pair's two ranks must plan identically, so they use the model)."""
+        if self.frozen:
+            return
         k = (bool(pre), int(g))
         old = self.meas.get(k)
         self.meas[k] = seconds if old is None else 0.75 * old + 0.25 * seconds
@@ -416,6 +505,10 @@ class _GammaPlanner:
         m = self.meas.get((bool(pre), int(g)))
         if m is not None:
             return m
+        if self.frozen:  # outside the table: linear in gamma from its largest entry
+            ks = [q for (p, q) in self.meas if p == bool(pre)] or [q for (_, q) in self.meas]
+            g0 = max(ks)
+            return self.meas.get((bool(pre), g0), self.meas.get((not pre, g0))) * g / g0
         model = self._model_time(pre, g)
         if self.meas:
             logs = [math.log(v / self._model_time(p, q)) for (p, q), v in self.meas.items()]
@@ -476,7 +569,7 @@ def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], c
     n0 = len(seq0)
     invt = inv_temp(cfg.temperature)
     gamma = planner.next_gamma() if planner else cfg.gamma
-    stats = _new_stats(gamma=gamma, gammas=[])
+    stats = _new_stats(gamma=gamma, gammas=[], step_log=[])
     rt.reset(seq0, stats)
     root = RandomStream(cfg.seed)
     tab_d = _Tables(rt, rt.u_draft, None if cfg.greedy else root.split(0), S_DCUR)
@@ -495,6 +588,7 @@ def decode_pearl(draft: LlamaModel, target: LlamaModel, prefix: Sequence[int], c
         stats["gammas"].append(gamma)
         key = ("pearl", k, gamma, m0, bool(cfg.greedy), invt, bool(concurrent))
         t_step = rt.replay(key, lambda: rt._pearl_body(k, gamma, m0, invt, cfg.greedy, concurrent), stats)
+        stats["step_log"].append((k == 0, gamma, m0, t_step))
         if planner is not None and m0 == 1:
             planner.observe_time(k == 0, gamma, t_step)
         s = rt.summary_host.numpy()

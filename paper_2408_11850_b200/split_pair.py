@@ -393,6 +393,7 @@ class _PlannerFromLink(_GammaPlanner):
         self.t_d = float(d["t_d"])
         self.t_t = {int(m): float(v) for m, v in t["t_t"].items()}
         self.meas = {}  # never fed: both ranks price steps with the shared model only
+        self.frozen = False
         self.gmax = gamma_max
         self.acc, self.exam = 3.0, 4.0
         self.gamma = gamma0
