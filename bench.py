@@ -4,10 +4,22 @@
 
 Workload (configs[1] of BASELINE.json): Llama-2-7B target + Llama-68M draft,
 random-init bf16 weights (controlled-alignment init, llama.py), batch 1,
-synthetic 128-token prompts, 128 new tokens, draft and target co-resident on
-one B200 (N=1).  A *step* is one ``decode_pearl`` call (prefill + decode of
-128 tokens) through the public API.  AR and fixed-gamma SD run on the same
-kernels in the same process for the speedup columns.
+synthetic 128-token prompts, 128 new tokens.  A *step* is one
+``decode_pearl`` call (prefill + decode of 128 tokens) through the public
+API.  AR and vanilla SD run on the same kernels in the same process.
+
+N = 1: draft and target co-resident on one B200.  PEARL (the headline) uses
+the adaptive draft length with a FROZEN planner calibration
+(profiles/planner_calib_*.json, so its gamma schedule depends on the tokens
+only) and its concurrent draft on a green-context SM partition; AR and SD
+run their target on the whole GPU.  Reported beside it: AR, SD at each
+fixed gamma (speedup_vs_sd divides by the BEST one), fixed-gamma PEARL, the
+gamma histogram, the per-decode spread and a T=0 leg.
+
+N >= 2 (torchrun): N/2 split pairs -- target on GPU 2i, draft on GPU 2i+1,
+one K6 draft->target exchange per step (split_pair.py) -- each decoding its
+own prompt shard; value = all pairs' tokens / max-over-ranks time
+(``--replicas``: co-resident replicas per GPU instead).
 
 Metric: generated tokens/s (whole job, all ranks), plus speedup vs AR and
 vs vanilla SD and mean accepted tokens per target forward.
@@ -15,10 +27,6 @@ vs vanilla SD and mean accepted tokens per target forward.
   e2e   = tokens / wall time of the public API calls (host prompt in, host
           tokens out: H2D of prompt + uniform tables, D2H of step summaries)
 Weights (13.6 GB) exceed L2 (126 MB), so every forward streams from HBM.
-
-N>1: one process per GPU (torchrun); each rank runs its own co-resident
-draft/target replica on its own prompt shard (replicas only, no data-path
-collective); value = all ranks' tokens / max-over-ranks time.
 
 --impl reference: the reference algorithm's CPU path (oracle/ port of
 pearl_lab's decode_pearl driving a PyTorch CPU Llama of the same
@@ -110,7 +118,60 @@ def _prompts(n, P, V, seed):
     return [rng.integers(2, V, P).tolist() for _ in range(n)]
 
 
+def _calib_path(pair, temp):
+    slug = pair.replace("/", "_")
+    return os.path.join(REPO, "profiles", f"planner_calib_{slug}_T{'0' if temp is None else f'{temp:g}'}.json")
+
+
+def planner_calibration(draft, target, args, prompt, greedy, temp):
+    """Frozen planner table (fastpath.PlannerCalibration): the committed one
+    for this pair (profiles/planner_calib_*.json, measured on B200) unless
+    --live-calibration; measured here otherwise and written to gpurun_out/.
+    Installed before any timed decode, so the adaptive gamma schedule is a
+    function of the decode's tokens only (reproducible across boxes)."""
+    from paper_2408_11850_b200 import fastpath
+    path = _calib_path(args.pair, 0.0 if greedy else temp)
+    if os.path.exists(path) and not args.live_calibration:
+        with open(path) as fh:
+            cal = fastpath.PlannerCalibration.from_json(json.load(fh), source=os.path.relpath(path, REPO))
+    else:
+        cal = fastpath.calibrate_planner(draft, target, prompt, args.gamma_max, temperature=temp, greedy=greedy,
+                                         new_tokens=min(96, args.new))
+        os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(REPO, "gpurun_out", os.path.basename(path)), "w") as fh:
+            json.dump(cal.to_json(), fh, indent=1)
+    fastpath.set_planner_calibration(draft, target, cal)
+    return cal
+
+
+def _leg_stats(res, kind, pk):
+    steps = [st for r in res for st in r.steps]
+    toks = [len(r.tokens) for r in res]
+    dev = [r.stats["device_s"] for r in res]
+    out = dict(tokens=sum(toks), device_s=sum(dev),
+               launches=sum(r.stats["launches"] for r in res),
+               replays=sum(r.stats.get("replays", 0) for r in res),
+               mean_tok_per_fwd=pk.mean_tokens_per_target_forward(steps),
+               alpha=pk.empirical_acceptance(steps) if kind != "ar" else None,
+               fallbacks=sum(r.stats.get("fallbacks", 0) for r in res),
+               per_decode=[t / d for t, d in zip(toks, dev) if d > 0])
+    gs = [g for r in res for g in r.stats.get("gammas", [])]
+    if gs:
+        hist = {}
+        for g in gs:
+            hist[str(g)] = hist.get(str(g), 0) + 1
+        out["gamma_hist"] = dict(sorted(hist.items(), key=lambda kv: int(kv[0])))
+    return out
+
+
+def _spread(v):
+    if not v:
+        return None
+    return {"min": round(min(v), 2), "median": round(statistics.median(v), 2), "max": round(max(v), 2)}
+
+
 def run_gpu(args):
+    """N = 1 (and --replicas): draft and target co-resident on each GPU."""
     import torch
     import torch.distributed as dist
 
@@ -122,101 +183,105 @@ def run_gpu(args):
         dist.init_process_group(backend, init_method="env://")
     local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    if ws >= 2 and ws % 2 == 0 and not args.replicas:
+        return run_split(args, ws, rank, local)
     import paper_2408_11850_b200 as pk
-    from paper_2408_11850_b200 import _lib, llama
+    from paper_2408_11850_b200 import llama
 
     align = llama.AlignSpec(branch_std=args.branch_std if args.branch_std is not None else PAIR_BRANCH_STD[args.pair],
                             kappa=args.kappa)
     sweep_bs = [int(b) for b in args.batch_sweep.split(",") if b] if args.batch_sweep else []
-    target, draft = llama.build_pair(args.pair, gemm_target=args.gemm_target, align=align,
-                                     n_slots=max([1] + sweep_bs),
-                                     max_seq=args.prompt + args.new + 2 * args.gamma_max + 16, max_tokens=128,
-                                     temperature=1.0 if args.temperature <= 0 else args.temperature,
-                                     draft_sms=args.draft_sms if args.draft_sms is not None
-                                     else int(os.environ.get("PEARL_DRAFT_SMS", PAIR_DRAFT_SMS[args.pair])))
     greedy = args.temperature <= 0
     temp = 1.0 if greedy else args.temperature
+    max_seq = args.prompt + args.new + 2 * args.gamma_max + 16
+    target, draft = llama.build_pair(args.pair, gemm_target=args.gemm_target, align=align, max_seq=max_seq,
+                                     max_tokens=128, temperature=temp, n_slots=max([1] + sweep_bs),
+                                     draft_sms=args.draft_sms if args.draft_sms is not None
+                                     else int(os.environ.get("PEARL_DRAFT_SMS", PAIR_DRAFT_SMS[args.pair])))
+    # AR and SD never overlap two models: they run on the target over the
+    # WHOLE GPU (its own stream-K grids), not on PEARL's partition
+    target_full = target.clone(sm_count=0) if getattr(target, "green_partition", None) is not None else target
     V = target.cfg.vocab
     draft_sms_used = getattr(target, "green_partition", (None, None, 0, 0))[2]
     prompts = _prompts(args.warmup + args.steps, args.prompt, V, seed=1000 + rank)
 
-    def cfg_for(gamma, seed, adaptive=False):
-        return pk.EngineConfig(gamma=gamma, max_new_tokens=args.new, seed=seed, greedy=greedy, temperature=temp,
+    def cfg_for(gamma, seed, adaptive=False, g=greedy):
+        return pk.EngineConfig(gamma=gamma, max_new_tokens=args.new, seed=seed, greedy=g, temperature=temp,
                                adaptive_gamma=adaptive, gamma_max=args.gamma_max)
 
-    pearl_gamma = args.gamma
+    cal = planner_calibration(draft, target, args, prompts[0], greedy, temp)
+    sd_gammas = [int(g) for g in args.sd_gammas.split(",")]
+    pearl_fixed = [int(g) for g in args.pearl_gammas.split(",") if g]
 
-    def run(kind, i):
+    def run(kind, i, g=greedy):
+        seed = 17 + i
         if kind == "pearl":
-            return pk.decode_pearl(draft, target, prompts[i], cfg_for(pearl_gamma, 17 + i, not args.fixed_gamma))
-        if kind == "sd":
-            return pk.decode_sd(draft, target, prompts[i], cfg_for(args.sd_gamma, 17 + i))
-        if kind in ("sd8", "sd16"):
-            return pk.decode_sd(draft, target, prompts[i], cfg_for(int(kind[2:]), 17 + i))
-        return pk.decode_autoregressive(target, prompts[i], cfg_for(1, 17 + i))
+            return pk.decode_pearl(draft, target, prompts[i], cfg_for(args.gamma, seed, True, g))
+        if kind.startswith("pearl"):
+            return pk.decode_pearl(draft, target, prompts[i], cfg_for(int(kind[5:]), seed, False, g))
+        if kind.startswith("sd"):
+            return pk.decode_sd(draft, target_full, prompts[i], cfg_for(int(kind[2:]), seed, False, g))
+        return pk.decode_autoregressive(target_full, prompts[i], cfg_for(1, seed, False, g))
 
-    results = {}
-    timed_results = {}
-    clocks = None
-    for kind in ("ar", "sd", "sd8", "sd16", "pearl"):  # PEARL last: its clocks are sampled
+    def leg(kind, g=greedy, clocks=False):
         for i in range(args.warmup):
-            run(kind, i)
+            run(kind, i, g)
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
-        if kind == "pearl":
-            clocks = Clocks(local)
+        ck = Clocks(local) if clocks else None
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         ev0.record()
-        res = [run(kind, args.warmup + i) for i in range(args.steps)]
+        res = [run(kind, args.warmup + i, g) for i in range(args.steps)]
         ev1.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        ev_s = ev0.elapsed_time(ev1) / 1e3
-        if kind == "pearl":
-            clocks = clocks.stop()
-        toks = sum(len(r.tokens) for r in res)
-        dev = sum(r.stats["device_s"] for r in res)
-        timed_results[kind] = res
-        steps = [s for r in res for s in r.steps]
-        results[kind] = dict(tokens=toks, device_s=dev, wall_s=wall, event_s=ev_s,
-                             launches=sum(r.stats["launches"] for r in res),
-                             replays=sum(r.stats.get("replays", 0) for r in res),
-                             mean_tok_per_fwd=pk.mean_tokens_per_target_forward(steps),
-                             alpha=pk.empirical_acceptance(steps) if kind != "ar" else None,
-                             gamma=res[0].stats.get("gamma"),
-                             gammas=sorted(set(g for r in res for g in r.stats.get("gammas", []))),
-                             fallbacks=sum(r.stats.get("fallbacks", 0) for r in res))
-    # max over ranks of the timed region, sum of tokens
-    agg = aggregate(results, ws)
-    # roofline of the dominant kernel sequence: one target window forward
-    rl = roofline(target, draft, args.gamma, args)
-    summary = run_summaries(target, draft, timed_results, args)
+        st = _leg_stats(res, kind, pk)
+        st.update(wall_s=wall, event_s=ev0.elapsed_time(ev1) / 1e3)
+        if ws > 1:
+            dist.barrier()
+        return st, res, (ck.stop() if ck else None)
+
+    results, timed = {}, {}
+    kinds = ["ar"] + [f"sd{g}" for g in sd_gammas] + [f"pearl{g}" for g in pearl_fixed] + ["pearl"]
+    clocks = None
+    for kind in kinds:  # adaptive PEARL (the headline) last: its clocks are sampled
+        results[kind], timed[kind], ck = leg(kind, clocks=kind == "pearl")
+        clocks = ck or clocks
+    greedy_leg = None
+    if args.greedy_leg and not greedy:
+        # BASELINE configs[1]: temperature 0 as well (greedy device path); the
+        # planner keeps the same frozen step-time table
+        g_res = {}
+        for kind in ["ar"] + [f"sd{g}" for g in sd_gammas] + ["pearl"]:
+            g_res[kind] = leg(kind, g=True)[0]
+        greedy_leg = summarize_legs(g_res, ws, sd_gammas, [])
+    agg = {k: aggregate_one(v, ws) for k, v in results.items()}
+    # dominant kernel sequence: the target window forward at the adaptive
+    # decodes' most frequent draft length (their post-verify window)
+    hist = results["pearl"].get("gamma_hist", {str(args.gamma): 1})
+    g_mode = int(max(hist.items(), key=lambda kv: kv[1])[0])
+    rl = roofline(target, draft, g_mode, args)
+    rl["by_window"] = {str(m): window_frac(target, m, args) for m in sorted({1, 4, g_mode, 16})}
+    summary = run_summaries(target, draft, timed, args)
     split_model = split_pair_model(target, draft, results["pearl"]["alpha"]) if ws == 1 else None
     target_bytes, draft_bytes = target.cfg.weight_bytes(), draft.cfg.weight_bytes()
-    sweep = batch_sweep(target, draft, args, sweep_bs, greedy, temp, ws) if sweep_bs else None
+    sweep = batch_sweep(target_full, draft, args, sweep_bs, greedy, temp, ws) if sweep_bs else None
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(target, draft, prompts[0], args, greedy, temp)
-    split = None
-    if ws >= 2 and ws % 2 == 0 and not args.no_split:
-        # the co-resident replicas are freed first: a split rank hosts one model
-        del target, draft
-        split = split_leg(args, ws, rank, greedy, temp, agg["ar"])
     if rank != 0:
         if ws > 1:
             dist.barrier()
             dist.destroy_process_group()
         return None
+    legs = summarize_legs(results, ws, sd_gammas, pearl_fixed, agg)
     wbytes = target_bytes + draft_bytes
     dp, ep, wp, tp = agg["pearl"]
-    da, ea, wa, ta = agg["ar"]
-    ds_, es, wsd, ts_ = agg["sd"]
-    value = tp / dp
     line = {
         "metric": METRIC,
-        "value": round(value, 2),
+        "value": round(tp / dp, 2),
         "unit": UNIT,
         "n_gpus": ws,
         "steps": args.steps,
@@ -228,41 +293,29 @@ def run_gpu(args):
         "dtype": "bf16",
         "data": "synthetic prompts (uniform random ids), random-init weights (controlled-alignment init)",
         "config": {
-            "workload": f"{args.pair} PEARL, batch 1, prompt {args.prompt}, {args.new} new tokens, "
-                        f"{'greedy T=0' if greedy else f'T={temp}'}, draft+target co-resident per GPU",
+            "workload": f"{args.pair} PEARL (adaptive draft length), batch 1, prompt {args.prompt}, "
+                        f"{args.new} new tokens, {'greedy T=0' if greedy else f'T={temp:g}'}, "
+                        f"draft+target co-resident per GPU",
             "pair": args.pair, "global_batch": ws, "prompt_len": args.prompt, "new_tokens": args.new,
-            "gamma": results["pearl"]["gammas"] if not args.fixed_gamma else args.gamma,
-            "adaptive_gamma": not args.fixed_gamma,
-            "sd_gamma": args.sd_gamma, "temperature": 0.0 if greedy else temp,
-            "target_gemm": args.gemm_target, "parallelism": f"replicas x{ws}",
-            "draft_sms": draft_sms_used,
+            "adaptive_gamma": True, "gamma_max": args.gamma_max,
+            "planner_calibration": cal.source, "temperature": 0.0 if greedy else temp,
+            "target_gemm": args.gemm_target, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+            "draft_sms": draft_sms_used, "ar_sd_target": "whole GPU (own stream-K grids)",
             "l2": f"weights {wbytes / 1e9:.2f} GB vs 126 MB L2: "
                   + ("every forward streams HBM (no flush needed)" if wbytes > 126e6 else "L2-resident (tiny pair)"),
         },
-        "e2e": {"value": round(tp / ep, 2), "unit": UNIT,
+        "e2e": {"value": round(tp / wp, 2), "unit": UNIT,
                 # per decode (one bench step): the prompt ids and the two uniform
                 # tables go up; one step summary (16 + gamma_max + 8 int32)
                 # comes back per step-graph replay
                 "h2d_bytes_per_step": 4 * (args.prompt + 1) + 8 * 2 * 4096,
                 "d2h_bytes_per_step": int(4 * (16 + args.gamma_max + 8) * results["pearl"]["replays"]
                                           / max(1, args.steps))},
-        "ar_tokens_per_s": round(ta / da, 2),
-        "sd_tokens_per_s": round(ts_ / ds_, 2),
-        "speedup_vs_ar": round((tp / dp) / (ta / da), 3),
-        "speedup_vs_sd": round((tp / dp) / (ts_ / ds_), 3),
-        "sd_best_tokens_per_s": round(max(agg[k][3] / agg[k][0] for k in ("sd", "sd8", "sd16")), 2),
-        "sd_by_gamma_tokens_per_s": {str(args.sd_gamma): round(ts_ / ds_, 2),
-                                     "8": round(agg["sd8"][3] / agg["sd8"][0], 2),
-                                     "16": round(agg["sd16"][3] / agg["sd16"][0], 2)},
-        "e2e_speedup_vs_ar": round((tp / ep) / (ta / ea), 3),
-        "mean_accepted_tokens_per_target_fwd": round(results["pearl"]["mean_tok_per_fwd"], 3),
-        "sd_mean_tokens_per_target_fwd": round(results["sd"]["mean_tok_per_fwd"], 3),
-        "alpha_hat": None if results["pearl"]["alpha"] is None else round(results["pearl"]["alpha"], 4),
-        "sd_alpha_hat": None if results["sd"]["alpha"] is None else round(results["sd"]["alpha"], 4),
+        **legs,
         "gpu_launches": int(results["pearl"]["launches"]),
         "exact_cdf_fallbacks": int(results["pearl"]["fallbacks"]),
+        "greedy_T0": greedy_leg,
         "roofline": rl,
-        "split_pair": split,
         "split_pair_model": split_model,
         "run_summary": summary,
         "batch_sweep": sweep,
@@ -273,6 +326,170 @@ def run_gpu(args):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+    return line
+
+
+def aggregate_one(r, ws):
+    return aggregate({"x": r}, ws)["x"]
+
+
+def summarize_legs(results, ws, sd_gammas, pearl_fixed, agg=None):
+    """tokens/s of every engine leg (device time, max over ranks) and the
+    speedup columns: PEARL (adaptive) over AR, over the BEST fixed-gamma SD
+    (and SD at gamma 4), and over the best fixed-gamma PEARL."""
+    agg = agg or {k: aggregate_one(v, ws) for k, v in results.items()}
+    tps = {k: a[3] / a[0] for k, a in agg.items()}
+    sd = {str(g): round(tps[f"sd{g}"], 2) for g in sd_gammas}
+    sd_best_g = max(sd_gammas, key=lambda g: tps[f"sd{g}"])
+    out = {
+        "ar_tokens_per_s": round(tps["ar"], 2),
+        "sd_by_gamma_tokens_per_s": sd,
+        "sd_best_tokens_per_s": round(tps[f"sd{sd_best_g}"], 2),
+        "sd_best_gamma": sd_best_g,
+        "speedup_vs_ar": round(tps["pearl"] / tps["ar"], 3),
+        "speedup_vs_sd": round(tps["pearl"] / tps[f"sd{sd_best_g}"], 3),
+        "speedup_vs_sd_gamma4": round(tps["pearl"] / tps["sd4"], 3) if "sd4" in tps else None,
+        "e2e_speedup_vs_ar": round((agg["pearl"][3] / agg["pearl"][2]) / (agg["ar"][3] / agg["ar"][2]), 3),
+        "mean_accepted_tokens_per_target_fwd": round(results["pearl"]["mean_tok_per_fwd"], 3),
+        "sd_mean_tokens_per_target_fwd": round(results[f"sd{sd_best_g}"]["mean_tok_per_fwd"], 3),
+        "alpha_hat": None if results["pearl"]["alpha"] is None else round(results["pearl"]["alpha"], 4),
+        "pearl_gamma_hist": results["pearl"].get("gamma_hist"),
+        "pearl_per_decode_tokens_per_s": _spread(results["pearl"]["per_decode"]),
+    }
+    if pearl_fixed:
+        pf = {str(g): round(tps[f"pearl{g}"], 2) for g in pearl_fixed}
+        best = max(pearl_fixed, key=lambda g: tps[f"pearl{g}"])
+        out.update({"pearl_fixed_by_gamma_tokens_per_s": pf, "pearl_fixed_best_gamma": best,
+                    "adaptive_vs_best_fixed_pearl": round(tps["pearl"] / tps[f"pearl{best}"], 3)})
+    else:
+        out["pearl_tokens_per_s"] = round(tps["pearl"], 2)
+    return out
+
+
+def run_split(args, ws, rank, local):
+    """N >= 2 (north_star placement): ranks (2i, 2i+1) form split pair i --
+    the target on the even GPU, the draft on the odd one, meeting through K6
+    mailboxes (NVLink peer memory, or copy-engine peer copies where the GPUs
+    cannot map each other).  Each pair decodes its own prompt shard (per-pair
+    prompts; per-prompt seeds as cli.py:94-96); tokens are counted once per
+    pair (target ranks), time is the max over all ranks.  Target ranks also
+    time single-GPU AR on the same prompts for the speedup column."""
+    import datetime
+    import torch
+    import torch.distributed as dist
+    import paper_2408_11850_b200 as pk
+    from paper_2408_11850_b200 import llama, split_pair
+
+    gloo = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=600))
+    role, peer = split_pair.pair_roles(rank, ws)
+    is_t = role == split_pair.ROLE_TARGET
+    tname, dname = llama.PAIRS[args.pair]
+    mc = llama.PRESETS[tname if is_t else dname]
+    align = llama.AlignSpec(branch_std=args.branch_std if args.branch_std is not None else PAIR_BRANCH_STD[args.pair],
+                            kappa=args.kappa)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    shared = llama._shared_tables(mc.vocab, align, dev)
+    w = llama.init_weights(mc, align, align.seed + (1 if is_t else 2), dev, shared)
+    del shared
+    greedy = args.temperature <= 0
+    temp = 1.0 if greedy else args.temperature
+    gemm = args.gemm_target if is_t else ("tcgen05" if mc.weight_bytes() > 1e9 else "cudacore")
+    model = llama.LlamaModel(mc, w, gemm=gemm, max_seq=args.prompt + args.new + 2 * args.gamma_max + 16,
+                             max_tokens=128 if gemm == "tcgen05" else 64, temperature=temp)
+    remote = split_pair.connect_pair(model, role, peer, gamma_max=args.gamma_max, group=gloo, timeout_s=120.0)
+    prompts = _prompts(args.warmup + args.steps, args.prompt, mc.vocab, seed=2000 + rank // 2)
+
+    def cfg_for(i, g, adaptive=True):
+        return pk.EngineConfig(gamma=args.gamma, max_new_tokens=args.new, seed=17 + i, greedy=g, temperature=temp,
+                               adaptive_gamma=adaptive, gamma_max=args.gamma_max)
+
+    def pearl(i, g=greedy):
+        c = cfg_for(i, g)
+        return pk.decode_pearl(remote, model, prompts[i], c) if is_t else pk.decode_pearl(model, remote, prompts[i], c)
+
+    def timed(fn, clocks=False, kind="pearl"):
+        for i in range(args.warmup):
+            fn(i)
+        torch.cuda.synchronize()
+        dist.barrier(group=gloo)
+        ck = Clocks(local) if clocks else None
+        t0 = time.perf_counter()
+        res = [fn(args.warmup + i) for i in range(args.steps)]
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        st = _leg_stats(res, kind, pk)
+        st.update(wall_s=wall, event_s=wall)
+        if not is_t:
+            st["tokens"] = 0  # counted once per pair, on its target rank
+        dist.barrier(group=gloo)
+        return st, res, (ck.stop() if ck else None)
+
+    try:
+        pst, pres, clocks = timed(pearl, clocks=rank == 0)
+        gst = timed(lambda i: pearl(i, True))[0] if args.greedy_leg and not greedy else None
+    finally:
+        remote.link.close()
+    # single-GPU AR on the target ranks, same prompts (the speedup baseline)
+    if is_t:
+        ast = timed(lambda i: pk.decode_autoregressive(model, prompts[i], cfg_for(i, greedy, False)), kind="ar")[0]
+    else:
+        dist.barrier(group=gloo)
+        dist.barrier(group=gloo)
+        ast = {"tokens": 0, "device_s": 0.0, "wall_s": 0.0, "event_s": 0.0}
+    rl = roofline(model, None, int(max((pst.get("gamma_hist") or {str(args.gamma): 1}).items(),
+                                       key=lambda kv: kv[1])[0]), args) if is_t else None
+    drl = draft_roofline(model, _peaks()[0]) if not is_t else None
+    ex_bytes = {"draft_to_target_per_step": "gamma x 4 B ids + gamma x V x 4 B q-logit rows (T > 0; ids only at T=0)",
+                "target_to_draft_per_step": 32}
+    agg_p = aggregate({"p": pst}, ws, device="cpu", group=gloo)["p"]
+    agg_a = aggregate({"a": ast}, ws, device="cpu", group=gloo)["a"]
+    agg_g = aggregate({"g": gst}, ws, device="cpu", group=gloo)["g"] if gst else None
+    gathered = [None] * ws
+    dist.all_gather_object(gathered, {"rank": rank, "role": role, "roofline": rl, "draft_roofline": drl,
+                                      "gamma_hist": pst.get("gamma_hist"), "alpha": pst["alpha"],
+                                      "mean_tok": pst["mean_tok_per_fwd"], "per_decode": pst["per_decode"]},
+                           group=gloo)
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return None
+    pairs = ws // 2
+    dp, ep, wp, tp = agg_p
+    da, ea, wa, ta = agg_a
+    value = tp / dp
+    ar_per_pair = (ta / da) / pairs
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * wp / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic prompts (uniform random ids), random-init weights (controlled-alignment init)",
+        "config": {"workload": f"{args.pair} PEARL, {pairs} split pair(s): target GPU 2i, draft GPU 2i+1, "
+                               f"batch 1 per pair, prompt {args.prompt}, {args.new} new tokens, "
+                               f"{'greedy T=0' if greedy else f'T={temp:g}'}, adaptive draft length",
+                   "pair": args.pair, "global_batch": pairs, "prompt_len": args.prompt, "new_tokens": args.new,
+                   "parallelism": f"split pairs x{pairs} (K6 draft->target exchange per step, no collective)",
+                   "gamma_max": args.gamma_max, "temperature": 0.0 if greedy else temp},
+        "e2e": {"value": round(tp / wp, 2), "unit": UNIT, "h2d_bytes_per_step": 4 * (args.prompt + 1) + 8 * 4096,
+                "d2h_bytes_per_step": 4 * (16 + args.gamma_max + 8)},
+        "ar_tokens_per_s": round(ta / da, 2),
+        "ar_tokens_per_s_per_gpu": round(ar_per_pair, 2),
+        "speedup_vs_ar": round((value / pairs) / ar_per_pair, 3),
+        "tokens_per_s_per_pair": round(value / pairs, 2),
+        "mean_accepted_tokens_per_target_fwd": round(statistics.mean(g["mean_tok"] for g in gathered if g["role"] == "target"), 3),
+        "alpha_hat": round(statistics.mean(g["alpha"] for g in gathered if g["role"] == "target"), 4),
+        "pearl_gamma_hist": gathered[0]["gamma_hist"],
+        "pearl_per_decode_tokens_per_s": _spread([x for g in gathered if g["role"] == "target" for x in g["per_decode"]]),
+        "greedy_T0": {"tokens_per_s": round(agg_g[3] / agg_g[0], 2)} if agg_g else None,
+        "exchange": ex_bytes,
+        "gpu_launches": int(pst["launches"]),
+        "roofline": gathered[0]["roofline"],
+        "draft_roofline": gathered[1]["draft_roofline"],
+        "cpu_baseline": None,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
     return line
 
 
@@ -287,9 +504,11 @@ def run_summaries(target, draft, timed, args):
     target.reset_adapter()
     draft.reset_adapter()
     out = {"t_draft_ms": round(params.t * 1e3, 4), "c": round(params.c, 2)}
-    for kind in ("pearl", "sd"):
-        if kind in timed:
-            out[kind] = metrics.summarize_run(kind, args.gamma if kind == "sd" else -1, timed[kind], params).to_dict()
+    sd_keys = [k for k in timed if k.startswith("sd")]
+    if "pearl" in timed:
+        out["pearl"] = metrics.summarize_run("pearl", -1, timed["pearl"], params).to_dict()
+    for k in sd_keys:
+        out[k] = metrics.summarize_run("sd", int(k[2:]), timed[k], params).to_dict()
     return out
 
 
@@ -374,98 +593,7 @@ def batch_sweep(target, draft, args, bs, greedy, temp, ws):
 SWEEP_GAMMAS = (4, 8, 16)
 
 
-def split_leg(args, ws, rank, greedy, temp, ar_agg):
-    """N >= 2: ranks (2i, 2i+1) form split pair i -- the target on the even
-    GPU, the draft on the odd one, meeting through K6 mailboxes (NVLink peer
-    memory).  Each pair decodes its own prompts; tokens are counted once per
-    pair (target ranks), time is the max over all ranks.
-
-    Guarded: every rank-local failure (including a K6 wait timing out) is
-    caught, all ranks agree on success through one collective, and the leg
-    reports {"error": ...} instead of taking the replica line down with it."""
-    import datetime
-    import torch
-    import torch.distributed as dist
-    import paper_2408_11850_b200 as pk
-    gloo = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=240))
-    err, local = None, None
-    try:
-        local = _split_local(args, ws, rank, greedy, temp, gloo)
-    except Exception as ex:  # noqa: BLE001 -- reported, never fatal
-        err = f"rank {rank}: {type(ex).__name__}: {str(ex)[:200]}"
-    flag = torch.tensor([1.0 if err else 0.0])
-    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=gloo)
-    if flag.item() > 0:
-        return {"error": err or "a peer rank failed"}
-    one, steps, gammas = local
-    d, e, wl, t = aggregate(one, ws)["pearl"]
-    ar_tps_per_gpu = ar_agg[3] / ar_agg[0] / ws
-    return {"pairs": ws // 2, "placement": "target on even GPU, draft on odd GPU, K6 NVLink mailboxes",
-            "tokens_per_s": round(t / d, 2), "e2e_tokens_per_s": round(t / e, 2),
-            "tokens_per_s_per_pair": round(t / d / (ws // 2), 2),
-            "speedup_vs_single_gpu_ar": round(t / d / (ws // 2) / ar_tps_per_gpu, 3),
-            "mean_accepted_tokens_per_target_fwd": round(pk.mean_tokens_per_target_forward(steps), 3),
-            "alpha_hat": round(pk.empirical_acceptance(steps), 4), "gammas": gammas}
-
-
-def _split_local(args, ws, rank, greedy, temp, gloo):
-    import gc
-    import torch
-    import torch.distributed as dist
-    import paper_2408_11850_b200 as pk
-    from paper_2408_11850_b200 import llama, split_pair
-
-    gc.collect()
-    torch.cuda.empty_cache()
-    role, peer = split_pair.pair_roles(rank, ws)
-    tname, dname = llama.PAIRS[args.pair]
-    mc = llama.PRESETS[tname if role == split_pair.ROLE_TARGET else dname]
-    need = mc.weight_bytes() * 1.1 + (2 << 30)
-    ok = torch.tensor([1.0 if torch.cuda.mem_get_info()[0] > need else 0.0])
-    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=gloo)
-    if ok.item() < 1:
-        raise RuntimeError("not enough free device memory after the replica leg")
-    align = llama.AlignSpec(branch_std=args.branch_std if args.branch_std is not None else PAIR_BRANCH_STD[args.pair],
-                            kappa=args.kappa)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    shared = llama._shared_tables(mc.vocab, align, dev)
-    is_t = role == split_pair.ROLE_TARGET
-    w = llama.init_weights(mc, align, align.seed + (1 if is_t else 2), dev, shared)
-    del shared
-    gemm = args.gemm_target if is_t else ("tcgen05" if mc.weight_bytes() > 1e9 else "cudacore")
-    model = llama.LlamaModel(mc, w, gemm=gemm, max_seq=args.prompt + args.new + 2 * args.gamma_max + 16,
-                             max_tokens=64, temperature=1.0 if greedy else temp)
-    remote = split_pair.connect_pair(model, role, peer, gamma_max=args.gamma_max, group=gloo, timeout_s=60.0)
-    prompts = _prompts(args.warmup + args.steps, args.prompt, mc.vocab, seed=2000 + rank // 2)
-
-    def run(i):
-        cfg = pk.EngineConfig(gamma=args.gamma, max_new_tokens=args.new, seed=17 + i, greedy=greedy, temperature=temp,
-                              adaptive_gamma=not args.fixed_gamma, gamma_max=args.gamma_max)
-        return pk.decode_pearl(remote, model, prompts[i], cfg) if is_t else pk.decode_pearl(model, remote, prompts[i],
-                                                                                             cfg)
-
-    try:
-        for i in range(args.warmup):
-            run(i)
-        torch.cuda.synchronize()
-        dist.barrier(group=gloo)
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        ev0.record()
-        res = [run(args.warmup + i) for i in range(args.steps)]
-        ev1.record()
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-    finally:
-        remote.link.close()
-    toks = sum(len(r.tokens) for r in res) if is_t else 0
-    steps = [s for r in res for s in r.steps]
-    one = {"pearl": dict(device_s=sum(r.stats["device_s"] for r in res), event_s=ev0.elapsed_time(ev1) / 1e3,
-                         wall_s=wall, tokens=toks)}
-    return one, steps, sorted(set(g for r in res for g in r.stats.get("gammas", [])))
-
-
-def aggregate(results, ws, device=None):
+def aggregate(results, ws, device=None, group=None):
     """(max device s, max event s, max wall s, sum tokens) per engine over ranks."""
     import torch
     import torch.distributed as dist
@@ -477,50 +605,71 @@ def aggregate(results, ws, device=None):
                             dtype=torch.float64)
         if ws > 1:
             mx = vals.clone()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
             sm = vals.clone()
-            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM, group=group)
             agg[kind] = (mx[0].item(), mx[1].item(), mx[2].item(), sm[3].item())
         else:
             agg[kind] = tuple(vals.tolist())
     return agg
 
 
+def _forward_time(model, M, ctx, n=10):
+    """CUDA-event time of one M-token window forward at position ctx, the
+    forward captured as a CUDA graph and replayed back to back (as inside a
+    decode step graph)."""
+    import torch
+    toks = torch.full((M,), 5, dtype=torch.int32, device="cuda")
+    pos = torch.tensor([ctx], dtype=torch.int32, device="cuda")
+    out = torch.empty(M, model.cfg.vocab, dtype=torch.float32, device="cuda")
+    for _ in range(2):
+        model.forward(toks, M, pos, 0, out)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        model.forward(toks, M, pos, 0, out)
+    for _ in range(2):
+        g.replay()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(n):
+        g.replay()
+    e.record()
+    e.synchronize()
+    model.reset_adapter()
+    return s.elapsed_time(e) / 1e3 / n
+
+
+def _forward_bytes(c, M, ctx):
+    return c.weight_bytes() + c.kv_bytes_per_token() * (ctx + M) + 4 * M * c.vocab
+
+
+def window_frac(target, M, args):
+    ctx = args.prompt + args.new // 2
+    t = _forward_time(target, M, ctx)
+    return {"ms": round(t * 1e3, 4), "frac": round(_forward_bytes(target.cfg, M, ctx) / t / 1e9 / _peaks()[0], 4)}
+
+
 def roofline(target, draft, gamma, args):
     """Dominant kernel sequence = one target window forward (M = gamma tokens).
 
     Algorithmic bytes per forward = bf16 weights + KV read over the context +
-    fp32 logits written; time = CUDA-event average of the forward on its
-    stream, after warm-up.
+    fp32 logits written; time = CUDA-event average of the forward (graph
+    replays on its stream), after warm-up.
     """
-    import torch
     peak, src = _peaks()
     M = max(1, int(gamma))
     ctx = args.prompt + args.new // 2
-    toks = torch.full((M,), 5, dtype=torch.int32, device="cuda")
-    pos = torch.tensor([ctx], dtype=torch.int32, device="cuda")
-    out = torch.empty(M, target.cfg.vocab, dtype=torch.float32, device="cuda")
-    for _ in range(3):
-        target.forward(toks, M, pos, 0, out)
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n = 10
-    s.record()
-    for _ in range(n):
-        target.forward(toks, M, pos, 0, out)
-    e.record()
-    e.synchronize()
-    t = s.elapsed_time(e) / 1e3 / n
+    t = _forward_time(target, M, ctx)
     c = target.cfg
-    byts = c.weight_bytes() + c.kv_bytes_per_token() * (ctx + M) + 4 * M * c.vocab
+    byts = _forward_bytes(c, M, ctx)
     achieved = byts / t / 1e9
     tr = _traffic().get(f"{c.name}_M{M}")
-    target.reset_adapter()
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": tr,
             "kernel": f"target window forward ({c.name}, M={M}, ctx={ctx}, {args.gemm_target} GEMMs)",
             "bytes_per_launch": int(byts), "ms_per_launch": round(t * 1e3, 4), "peak_source": src,
             "gemm_kernel": gemm_roofline(target, M, peak) if args.gemm_target == "tcgen05" else None,
-            "draft_forward": draft_roofline(draft, peak)}
+            "draft_forward": draft_roofline(draft, peak) if draft is not None else None}
 
 
 def draft_roofline(draft, peak):
@@ -673,13 +822,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pair", default="llama2-7b/68m")
-    ap.add_argument("--gamma", type=int, default=4)
-    ap.add_argument("--sd-gamma", type=int, default=4)
+    ap.add_argument("--gamma", type=int, default=4, help="initial draft length of adaptive PEARL")
+    ap.add_argument("--sd-gammas", default="4,8,16", help="fixed draft lengths of the vanilla SD legs")
+    ap.add_argument("--pearl-gammas", default="4,8,16,24", help="fixed draft lengths of the fixed-gamma PEARL legs")
     ap.add_argument("--gamma-max", type=int, default=32)
-    ap.add_argument("--fixed-gamma", action="store_true", help="PEARL with fixed --gamma instead of adaptive")
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--new", type=int, default=128)
     ap.add_argument("--temperature", type=float, default=1.0)
+    ap.add_argument("--greedy-leg", type=int, default=1, help="also time T=0 (BASELINE configs[1] asks T in {0, 1})")
+    ap.add_argument("--live-calibration", action="store_true",
+                    help="measure the adaptive planner's step-time table now instead of loading profiles/")
     ap.add_argument("--branch-std", type=float, default=None,
                     help="alignment knob (default per pair, calibrated to alpha-hat ~0.9 at T=1: tools/calib_alpha.py)")
     ap.add_argument("--kappa", type=float, default=13.0)
@@ -689,7 +841,8 @@ def main():
     ap.add_argument("--cpu-new", type=int, default=16)
     ap.add_argument("--cpu-prompt", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-split", action="store_true", help="N>=2: skip the split-pair (draft GPU / target GPU) leg")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>=2: co-resident replicas per GPU instead of split pairs")
     ap.add_argument("--sweep-gammas", default=",".join(str(g) for g in SWEEP_GAMMAS),
                     help="C5: fixed draft lengths tried per engine and batch size")
     ap.add_argument("--batch-sweep", default="1,4,16,32",

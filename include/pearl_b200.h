@@ -360,6 +360,21 @@ typedef struct {
  * ++(*send_seq) into its flag (system-scope fence before the flag store). */
 int pearl_xfer_send(const pearl_xfer_send_args* args, void* stream);
 
+/* Copy-engine push for GPU pairs that cannot map each other's memory
+ * (cudaDeviceCanAccessPeer == 0; also PEARL_K6_COPY=1 for tests): the same
+ * message as pearl_xfer_send, moved by stream-ordered cudaMemcpyAsync --
+ * payload first, then the new sequence number (computed on the device into
+ * the sender's 8-byte `staging` word) into the peer's flag, so the flag can
+ * only land after the payload.  Graph-capturable (memcpy nodes). */
+int pearl_xfer_send_copy(const pearl_xfer_send_args* args, unsigned long long* staging, void* stream);
+
+/* 1 if a kernel on the current device can store into memory of the device
+ * whose PCI bus id is `peer_pci_bus_id` (same device or peer access
+ * supported), 0 if not, negative on error. */
+int pearl_peer_storable(const char* peer_pci_bus_id);
+/* PCI bus id of the current device into out (>= 16 bytes). */
+int pearl_pci_bus_id(char* out, int len);
+
 /* One receive: spin (acquire, system scope) until the local mailbox's flag
  * reaches ++(*recv_seq), then copy n_ids ids out of it into dst_ids.  If
  * timeout_ns > 0 and the flag does not arrive in time, *status (optional)

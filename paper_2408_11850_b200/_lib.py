@@ -82,6 +82,9 @@ SIGNATURES = {
     "pearl_ipc_import": (_i32, [_vp, _vp]),
     "pearl_ipc_close": (_i32, [_vp]),
     "pearl_xfer_send": (_i32, [_vp, _vp]),
+    "pearl_xfer_send_copy": (_i32, [_vp, _vp, _vp]),
+    "pearl_peer_storable": (_i32, [ctypes.c_char_p]),
+    "pearl_pci_bus_id": (_i32, [ctypes.c_char_p, _i32]),
     "pearl_xfer_wait": (_i32, [_vp, _vp, _vp, _i32, _vp, ctypes.c_longlong, _vp]),
 }
 

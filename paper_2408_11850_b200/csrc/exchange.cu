@@ -173,6 +173,53 @@ extern "C" int pearl_xfer_send(const pearl_xfer_send_args* args, void* stream) {
   return PEARL_OK;
 }
 
+__global__ void xfer_seq_kernel(unsigned long long* send_seq, unsigned long long* staging) {
+  const unsigned long long seq = *send_seq + 1ull;
+  *send_seq = seq;
+  *staging = seq;
+}
+
+extern "C" int pearl_xfer_send_copy(const pearl_xfer_send_args* a, unsigned long long* staging, void* stream) {
+  PEARL_ARG_CHECK(a && a->peer_box && a->send_seq && staging, "bad xfer_send_copy arguments");
+  PEARL_ARG_CHECK(a->n_ids >= 0 && a->n_ids <= PEARL_MAILBOX_MAX_IDS && (a->n_ids == 0 || a->ids),
+                  "xfer_send_copy: 0 <= n_ids <= PEARL_MAILBOX_MAX_IDS");
+  PEARL_ARG_CHECK(a->n_rows >= 0 && (a->n_rows == 0 || (a->rows && a->V > 0)), "xfer_send_copy: rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* box = static_cast<char*>(a->peer_box);
+  if (a->n_ids)
+    PEARL_CUDA_TRY(cudaMemcpyAsync(box + PEARL_MAILBOX_IDS_OFFSET, a->ids, static_cast<size_t>(a->n_ids) * 4,
+                                   cudaMemcpyDefault, st));
+  if (a->n_rows)
+    PEARL_CUDA_TRY(cudaMemcpyAsync(box + PEARL_MAILBOX_ROWS_OFFSET, a->rows,
+                                   static_cast<size_t>(a->n_rows) * a->V * sizeof(float), cudaMemcpyDefault, st));
+  xfer_seq_kernel<<<1, 1, 0, st>>>(a->send_seq, staging);
+  PEARL_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  PEARL_CUDA_TRY(cudaMemcpyAsync(box, staging, sizeof(unsigned long long), cudaMemcpyDefault, st));
+  return PEARL_OK;
+}
+
+extern "C" int pearl_pci_bus_id(char* out, int len) {
+  PEARL_ARG_CHECK(out && len >= 16, "pci bus id buffer too small");
+  int dev = 0;
+  PEARL_CUDA_TRY(cudaGetDevice(&dev));
+  PEARL_CUDA_TRY(cudaDeviceGetPCIBusId(out, len, dev));
+  return PEARL_OK;
+}
+
+extern "C" int pearl_peer_storable(const char* peer_pci_bus_id) {
+  PEARL_ARG_CHECK(peer_pci_bus_id, "null pci bus id");
+  int dev = 0, peer = -1, ok = 0;
+  PEARL_CUDA_TRY(cudaGetDevice(&dev));
+  if (cudaDeviceGetByPCIBusId(&peer, peer_pci_bus_id) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;  // the peer GPU is not visible to this process: no direct stores
+  }
+  if (peer == dev) return 1;
+  PEARL_CUDA_TRY(cudaDeviceCanAccessPeer(&ok, dev, peer));
+  return ok ? 1 : 0;
+}
+
 extern "C" int pearl_xfer_wait(const void* box, unsigned long long* recv_seq, int32_t* dst_ids, int n_ids,
                                int32_t* status, long long timeout_ns, void* stream) {
   PEARL_ARG_CHECK(box && recv_seq, "bad xfer_wait arguments");

@@ -377,6 +377,14 @@ class LlamaModel(SequenceModel):
     def reset_adapter(self) -> None:
         self._cached = []
 
+    def clone(self, sm_count: int = 0, n_slots: Optional[int] = None) -> "LlamaModel":
+        """A second device model over the SAME weight tensors (no copy) with its
+        own KV cache and workspace -- e.g. the target on the whole GPU for AR /
+        SD next to the SM-partitioned one PEARL's concurrent step uses."""
+        return LlamaModel(self.cfg, self.w, gemm=self.gemm, max_seq=self.max_seq, max_tokens=self.max_tokens,
+                          temperature=self.temperature, bos_id=self.bos_id, latency=self._latency,
+                          sm_count=sm_count, n_slots=self.n_slots if n_slots is None else n_slots)
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             _lib.load().pearl_llama_destroy(self.handle)

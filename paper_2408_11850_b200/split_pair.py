@@ -39,6 +39,7 @@ once when the link connects, so both planners make the same choices.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import replace
 from typing import Dict, List, Optional, Sequence
 
@@ -74,7 +75,10 @@ class SplitLink:
         self.timeout_ns = int(timeout_s * 1e9)
         dev = torch.device("cuda", torch.cuda.current_device())
         # send_seq, recv_seq (uint64 as int64), arrive (uint32 in an int64 slot)
-        self.counters = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)  # send, recv, arrive, staging
+        # K6 transport: direct peer stores when this GPU can map the peer's
+        # memory (NVLink / NVSwitch, or the same device), else copy-engine pushes
+        self.mode = "peer_store"
         self.closed = False
 
     @classmethod
@@ -96,13 +100,20 @@ class SplitLink:
         _lib.check(lib.pearl_mailbox_alloc(nbytes, ctypes.byref(p)), "pearl_mailbox_alloc")
         handle = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
         _lib.check(lib.pearl_ipc_export(p, handle), "pearl_ipc_export")
+        bus = ctypes.create_string_buffer(64)
+        _lib.check(lib.pearl_pci_bus_id(bus, 64), "pearl_pci_bus_id")
         entry = {"role": role, "rank": dist.get_rank(), "handle": handle.raw, "vocab": int(vocab),
-                 "gamma_max": int(gamma_max), "info": dict(local_info)}
+                 "gamma_max": int(gamma_max), "info": dict(local_info), "pci": bus.value.decode()}
         peer = exchange_entries(entry, peer_rank, group)
+        storable = int(lib.pearl_peer_storable(peer["pci"].encode()))
+        if storable < 0:
+            _lib.check(storable, "pearl_peer_storable")
         q = ctypes.c_void_p()
         hbuf = ctypes.create_string_buffer(peer["handle"], _lib.IPC_HANDLE_BYTES)
         _lib.check(lib.pearl_ipc_import(hbuf, ctypes.byref(q)), "pearl_ipc_import")
         link = cls(role, peer_rank, vocab, gamma_max, p.value, q.value, peer["info"], timeout_s)
+        if storable == 0 or os.environ.get("PEARL_K6_COPY", "0") == "1":
+            link.mode = "copy_engine"
         # both sides have mapped each other's mailbox before the first push
         dist.barrier(group=group)
         return link
@@ -122,6 +133,10 @@ class SplitLink:
     def send(self, ids_addr: int, n_ids: int, rows_addr: Optional[int], n_rows: int, stream) -> None:
         a = _XferArgs(self.peer_box, ids_addr, int(n_ids), rows_addr, int(n_rows), self.V, self._ctr(0),
                       self._ctr(2))
+        if self.mode == "copy_engine":
+            _lib.check(_lib.load().pearl_xfer_send_copy(ctypes.byref(a), self._ctr(3), _device.stream_ptr(stream)),
+                       "pearl_xfer_send_copy")
+            return
         _lib.check(_lib.load().pearl_xfer_send(ctypes.byref(a), _device.stream_ptr(stream)), "pearl_xfer_send")
 
     def wait(self, dst_addr: Optional[int], n_ids: int, status_addr: int, stream) -> None:

@@ -51,3 +51,32 @@ def test_reference_arm_line():
              "--cpu-prompt", "16")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] in ("port", "reference")
+
+
+def test_bench_split_pairs_four_ranks_one_gpu():
+    """N = 4 under torchrun: two split pairs (targets on ranks 0 / 2, drafts
+    on 1 / 3) -- functional run with all ranks on cuda:0 over gloo
+    (PEARL_BENCH_BACKEND=gloo); rank 0 prints one line whose value counts
+    both pairs' tokens."""
+    import socket
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, PEARL_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "4",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(REPO, "bench.py"),
+                          "--gpus", "4", "--pair", "tiny", "--steps", "2", "--warmup", "1", "--new", "24",
+                          "--gamma-max", "8"], capture_output=True, text=True, timeout=900, cwd=REPO, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    for k in REQUIRED:
+        assert k in d, k
+    assert d["n_gpus"] == 4 and d["config"]["global_batch"] == 2
+    assert "split pairs x2" in d["config"]["parallelism"]
+    assert d["value"] > 0 and d["speedup_vs_ar"] > 0
+    assert d["roofline"]["frac"] > 0 and d["draft_roofline"]["us_per_launch"] > 0

@@ -50,10 +50,12 @@ def _cases():
     return out
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, mode="peer_store"):
     try:
         sys.path.insert(0, REPO)
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2")
+        if mode == "copy_engine":
+            os.environ["PEARL_K6_COPY"] = "1"
         import torch.distributed as dist
         torch.cuda.set_device(0)
         dist.init_process_group("gloo", init_method="env://")
@@ -63,6 +65,7 @@ def _worker(rank, port, q):
         target, draft = llama.build_pair("tiny", gemm_target="tcgen05", max_seq=256, max_tokens=32)
         local = target if role == split.ROLE_TARGET else draft
         remote = split.connect_pair(local, role, peer, gamma_max=8, timeout_s=60.0)
+        assert remote.link.mode == mode, remote.link.mode
         outs = []
         for pr, cfg in _cases():
             if role == split.ROLE_TARGET:
@@ -79,15 +82,18 @@ def _worker(rank, port, q):
         q.put((rank, None, traceback.format_exc()))
 
 
-@pytest.fixture(scope="module")
-def split_results():
+@pytest.fixture(scope="module", params=["peer_store", "copy_engine"])
+def split_results(request):
+    """Both K6 transports: direct peer stores (NVLink / same device) and the
+    copy-engine fallback for GPUs that cannot map each other (forced here
+    with PEARL_K6_COPY=1)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, request.param)) for r in range(2)]
     for p in procs:
         p.start()
     got = {}
@@ -172,3 +178,46 @@ def test_exchange_push_then_wait_same_process():
         assert torch.equal(got.view(3, V), rows.cpu())
     finally:
         lib.pearl_mailbox_free(box)
+
+
+def test_exchange_copy_engine_push_then_wait():
+    """The copy-engine push (pearl_xfer_send_copy) delivers ids, rows and the
+    sequence flag in order, like the peer-store kernel."""
+    import ctypes
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2408_11850_b200 import _lib, split_pair
+    lib = _lib.load()
+    V = 48
+    box = ctypes.c_void_p()
+    _lib.check(lib.pearl_mailbox_alloc(int(lib.pearl_mailbox_bytes(2, V)), ctypes.byref(box)), "alloc")
+    try:
+        ctr = torch.zeros(4, dtype=torch.int64, device="cuda")  # send, recv, arrive, staging
+        st = torch.cuda.current_stream().cuda_stream
+        for it in range(3):
+            ids = torch.arange(4, dtype=torch.int32, device="cuda") + 100 * it
+            rows = torch.randn(2, V, device="cuda")
+            a = split_pair._XferArgs(box.value, ids.data_ptr(), 4, rows.data_ptr(), 2, V, ctr.data_ptr(),
+                                     ctr.data_ptr() + 16)
+            _lib.check(lib.pearl_xfer_send_copy(ctypes.byref(a), ctr.data_ptr() + 24, st), "send_copy")
+            dst = torch.zeros(4, dtype=torch.int32, device="cuda")
+            status = torch.zeros(1, dtype=torch.int32, device="cuda")
+            _lib.check(lib.pearl_xfer_wait(box, ctr.data_ptr() + 8, dst.data_ptr(), 4, status.data_ptr(), int(5e9),
+                                           st), "wait")
+            torch.cuda.synchronize()
+            assert int(status.item()) == 0 and torch.equal(dst, ids)
+            assert ctr[0].item() == it + 1 and ctr[1].item() == it + 1 and ctr[3].item() == it + 1
+    finally:
+        lib.pearl_mailbox_free(box)
+
+
+def test_peer_storable_same_device():
+    import ctypes
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2408_11850_b200 import _lib
+    lib = _lib.load()
+    bus = ctypes.create_string_buffer(64)
+    _lib.check(lib.pearl_pci_bus_id(bus, 64), "pci")
+    assert lib.pearl_peer_storable(bus.value) == 1
+    assert lib.pearl_peer_storable(b"0000:ff:1f.0") == 0  # not a visible device
