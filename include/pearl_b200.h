@@ -174,6 +174,9 @@ int pearl_residual(const double* p, const double* q, int V, double* out, int32_t
 /* Linear-layer engine of a model. */
 #define PEARL_GEMM_CUDACORE 0 /* batch-invariant 128-bit GEMV (draft, K2) */
 #define PEARL_GEMM_TCGEN05 1  /* tcgen05 + TMA small-M contraction (target, K3) */
+/* OR-ed into pearl_gemm's kind (tcgen05 only): W is stored tile-major,
+ * [N/128][K/64][128][64] bf16, so every 128x64 TMA box is 16 contiguous KB */
+#define PEARL_GEMM_W_TILED 0x100
 
 typedef struct {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, vocab;

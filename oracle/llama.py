@@ -38,8 +38,28 @@ def _bf(x: torch.Tensor, on: bool) -> torch.Tensor:
     return x.to(torch.bfloat16).to(torch.float32) if on else x
 
 
-def rope_tables(hd: int, max_seq: int, theta: float):
-    inv = theta ** (-np.arange(0, hd, 2, dtype=np.float64) / hd)
+def _scaled_inv_freq(inv: np.ndarray, scaling) -> np.ndarray:
+    """Hugging Face's rope_scaling rules, branch by branch (linear: every
+    frequency / factor; llama3: low band / factor, high band kept, the middle
+    band interpolated in original_context / wavelength)."""
+    if scaling is None:
+        return inv
+    if scaling[0] == "linear":
+        return inv / scaling[1]
+    _, factor, lo, hi, ctx = scaling
+    out = inv.copy()
+    for i, f in enumerate(inv):
+        wl = 2 * math.pi / f
+        if wl > ctx / lo:
+            out[i] = f / factor
+        elif wl >= ctx / hi:
+            s = (ctx / wl - lo) / (hi - lo)
+            out[i] = (1 - s) * f / factor + s * f
+    return out
+
+
+def rope_tables(hd: int, max_seq: int, theta: float, scaling=None):
+    inv = _scaled_inv_freq(theta ** (-np.arange(0, hd, 2, dtype=np.float64) / hd), scaling)
     ang = np.arange(max_seq, dtype=np.float64)[:, None] * inv[None, :]
     return torch.from_numpy(np.cos(ang).astype(np.float32)), torch.from_numpy(np.sin(ang).astype(np.float32))
 
@@ -69,7 +89,7 @@ class OracleLlama:
         self.lm_head = mv(weights["lm_head"])
         self.final_norm = weights["final_norm"].to(self.dev).float()
         self.layers = [{k: mv(v) for k, v in L.items()} for L in weights["layers"]]
-        self.cos, self.sin = rope_tables(cfg.head_dim, max_seq, cfg.rope_theta)
+        self.cos, self.sin = rope_tables(cfg.head_dim, max_seq, cfg.rope_theta, getattr(cfg, "rope_scaling", None))
         self.cos, self.sin = self.cos.to(self.dev), self.sin.to(self.dev)
         L, KV, hd = cfg.n_layers, cfg.n_kv_heads, cfg.head_dim
         self.kc = torch.zeros(L, max_seq, KV, hd, device=self.dev)

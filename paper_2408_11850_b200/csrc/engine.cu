@@ -45,11 +45,14 @@ __global__ void commit_kernel(pearl_commit_args a) {
   // carry the unverified fresh drafts' q rows over as the next pending block
   // (pending_rows == NULL: the draft rank of a split pair, which keeps no q rows)
   if (!a.sd_mode && full_accept && a.pending_rows && blockIdx.x < a.gamma - 1) {
-    const float4* src = reinterpret_cast<const float4*>(a.draft_rows + static_cast<size_t>(blockIdx.x + 1) * a.V);
-    float4* dst = reinterpret_cast<float4*>(a.pending_rows + static_cast<size_t>(blockIdx.x) * a.V);
-    for (int i = threadIdx.x; i < a.V / 4; i += blockDim.x) dst[i] = src[i];
-    for (int i = (a.V / 4) * 4 + threadIdx.x; i < a.V; i += blockDim.x)
-      a.pending_rows[static_cast<size_t>(blockIdx.x) * a.V + i] = a.draft_rows[static_cast<size_t>(blockIdx.x + 1) * a.V + i];
+    const float* srow = a.draft_rows + static_cast<size_t>(blockIdx.x + 1) * a.V;
+    float* drow = a.pending_rows + static_cast<size_t>(blockIdx.x) * a.V;
+    // rows start 16-byte aligned only when V % 4 == 0 (e.g. not V = 32001)
+    const int nvec = (a.V % 4 == 0) ? a.V / 4 : 0;
+    const float4* src = reinterpret_cast<const float4*>(srow);
+    float4* dst = reinterpret_cast<float4*>(drow);
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = src[i];
+    for (int i = nvec * 4 + threadIdx.x; i < a.V; i += blockDim.x) drow[i] = srow[i];
   }
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   pearl_seq_state s = *a.state;

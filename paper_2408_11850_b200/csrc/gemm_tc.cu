@@ -40,10 +40,20 @@ struct TcArgs {
   long long T;   // total (tile, k-block) iterations
   int G;         // CTAs sharing them (stream-K); a function of (N, K) only
   int seg_max;   // partial slots per tile
+  int w_tiled;   // W stored tile-major: [tiles][KB][128 rows][64 cols], one 16 KB box contiguous
   EpiArgs e;
   float* partials;
   int* flags;
 };
+
+// W tile (tile, kb): row-major [N, K] -> box at (k = 64 kb, row = 128 tile);
+// tile-major -> the 128 consecutive 128-byte rows at row (tile KB + kb) 128
+// (a contiguous 16 KB: a CTA's run of k-blocks streams one contiguous range)
+__device__ __forceinline__ void tma_load_w(void* dst, const CUtensorMap* map, uint64_t* bar, const TcArgs& a, int tile,
+                                           int kb) {
+  if (a.w_tiled) tma_load_2d(dst, map, bar, 0, (tile * a.KB + kb) * kTileN);
+  else tma_load_2d(dst, map, bar, kb * kTileK, tile * kTileN);
+}
 
 // ---- kernel ------------------------------------------------------------------
 template <int NT>
@@ -110,7 +120,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
       for (int it = 0; it < npre; ++it) {
         unsigned char* st = smem + it * stage_bytes;
         mbar_expect_tx(&full[it], bytes);
-        tma_load_2d(st, &tmW, &full[it], kb * kTileK, tile * kTileN);
+        tma_load_w(st, &tmW, &full[it], a, tile, kb);
         if (++kb == a.KB) { kb = 0; ++tile; }
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -127,7 +137,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         unsigned char* st = smem + s * stage_bytes;
         const int kc = kb * kTileK;
         mbar_expect_tx(&full[s], bytes);
-        tma_load_2d(st, &tmW, &full[s], kc, tile * kTileN);
+        tma_load_w(st, &tmW, &full[s], a, tile, kb);
         for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
         if (++kb == a.KB) { kb = 0; ++tile; }
       }
@@ -388,7 +398,7 @@ void tc_free(TcGemmCtx& ctx) {
 }
 
 int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int M, int N, int K, const EpiArgs& e,
-            cudaStream_t st, int force_splits) {
+            cudaStream_t st, int force_splits, bool w_tiled) {
   if (M < 1 || M > kMaxTokTiles * kTokTile) {
     set_error("tc_gemm: M must be in [1, 128]");
     return PEARL_ERR_ARG;
@@ -397,11 +407,17 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
     set_error("tc_gemm: K must be a multiple of 8");
     return PEARL_ERR_ARG;
   }
-  const auto key = std::make_tuple(static_cast<const void*>(W), N, K);
+  if (w_tiled && (N % kTileN != 0 || K % kTileK != 0)) {
+    set_error("tc_gemm: tile-major weights need N % 128 == 0 and K % 64 == 0");
+    return PEARL_ERR_ARG;
+  }
+  const auto key = std::make_tuple(static_cast<const void*>(W), w_tiled ? -N : N, K);
   auto it = ctx.wmaps.find(key);
   if (it == ctx.wmaps.end()) {
     TcWeightMap wm;
-    int rc = encode_2d(&wm.map, W, K, N, kTileN);
+    // tile-major: a [N K / 64, 64] matrix of 128-byte rows, box 64 x 128
+    int rc = w_tiled ? encode_2d(&wm.map, W, kTileK, static_cast<int>(static_cast<long long>(N) * K / kTileK), kTileN)
+                     : encode_2d(&wm.map, W, K, N, kTileN);
     if (rc) return rc;
     it = ctx.wmaps.emplace(key, wm).first;
   }
@@ -417,6 +433,7 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.T = static_cast<long long>(tiles) * a.KB;
   a.G = static_cast<int>(std::min<long long>(force_splits > 0 ? force_splits : ctx.num_sms, a.T));
   a.seg_max = tc_seg_max(tiles, a.KB, a.G);
+  a.w_tiled = w_tiled ? 1 : 0;
   a.e = e;
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;

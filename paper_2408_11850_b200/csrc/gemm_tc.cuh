@@ -41,7 +41,7 @@ struct TcGemmCtx {
 int tc_init(TcGemmCtx& ctx, const pearl_llama_config& cfg);
 void tc_free(TcGemmCtx& ctx);
 int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int M, int N, int K,
-            const EpiArgs& e, cudaStream_t st, int force_grid = 0);
+            const EpiArgs& e, cudaStream_t st, int force_grid = 0, bool w_tiled = false);
 // number of K splits the (legacy round-robin) planner picks for an (N, K) GEMM
 int tc_splits(int N, int K, int num_sms);
 // most stream-K segments any tile of an (tiles x KB) GEMM is cut into over G CTAs

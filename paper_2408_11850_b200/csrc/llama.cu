@@ -570,6 +570,9 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
   PEARL_ARG_CHECK(c.max_tokens >= 1 && c.max_tokens <= (c.gemm_kind == PEARL_GEMM_TCGEN05 ? 128 : 64),
                   "max_tokens in [1, 128] (tcgen05) / [1, 64] (CUDA-core)");
   PEARL_ARG_CHECK(c.max_seq >= 1 && c.max_seq <= 4096, "max_seq in [1, 4096]");
+  // logits / q rows are read and written with 16-byte vectors (GEMM epilogue,
+  // commit, K6): every row must start 16-byte aligned
+  PEARL_ARG_CHECK(c.vocab >= 2 && c.vocab % 4 == 0, "vocab must be a multiple of 4 (16-byte aligned logits rows)");
   Llama* m = new Llama();
   m->cfg = c;
   m->embed = static_cast<const bf16*>(ptrs[0]);
@@ -652,8 +655,12 @@ extern "C" int pearl_gemm(int kind, const void* W, const void* X, float* Y, int 
   e.out_f32 = Y;
   e.ld = N;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (kind == PEARL_GEMM_CUDACORE)
+  const bool w_tiled = (kind & PEARL_GEMM_W_TILED) != 0;
+  kind &= ~PEARL_GEMM_W_TILED;
+  if (kind == PEARL_GEMM_CUDACORE) {
+    PEARL_ARG_CHECK(!w_tiled, "the CUDA-core GEMV takes row-major weights");
     return launch_gemv(static_cast<const bf16*>(W), static_cast<const bf16*>(X), M, N, K, e, st);
+  }
   std::lock_guard<std::mutex> lk(g_gemm_mu);
   if (!g_gemm_ctx.partials) {
     pearl_llama_config c{};
@@ -669,7 +676,8 @@ extern "C" int pearl_gemm(int kind, const void* W, const void* X, float* Y, int 
     int rc = tc_init(g_gemm_ctx, c);
     if (rc) return rc;
   }
-  return tc_gemm(g_gemm_ctx, static_cast<const bf16*>(W), static_cast<const bf16*>(X), M, N, K, e, st, splits);
+  return tc_gemm(g_gemm_ctx, static_cast<const bf16*>(W), static_cast<const bf16*>(X), M, N, K, e, st, splits,
+                 w_tiled);
 }
 
 extern "C" int pearl_gemm_splits(int N, int K) {

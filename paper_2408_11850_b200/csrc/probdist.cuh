@@ -140,8 +140,11 @@ struct ClusterCtx {
   int parity;
 };
 
+// Non-.aligned cluster barrier: callers may arrive from divergent code
+// (e.g. after a thread-0-only block), which the .aligned form used by
+// cg::cluster_group::sync() does not allow (compute-sanitizer synccheck).
 __device__ __forceinline__ void cluster_sync_all() {
-  cg::this_cluster().sync();
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
 }
 
 // Gather up to 4 values from every CTA of the cluster.  After the cluster

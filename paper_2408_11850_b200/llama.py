@@ -57,6 +57,11 @@ class LlamaConfig:
     vocab: int
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
+    # ("linear", factor) or ("llama3", factor, low_freq_factor, high_freq_factor,
+    # original_max_position_embeddings); None = plain RoPE (checkpoint.config_from_hf)
+    rope_scaling: Optional[tuple] = None
+    bos_id: int = 1
+    eos_id: Optional[int] = None
 
     @property
     def head_dim(self) -> int:
@@ -122,8 +127,28 @@ class AlignSpec:
     seed: int = 1234
 
 
-def rope_tables(hd: int, max_seq: int, theta: float):
+def rope_inv_freq(hd: int, theta: float, scaling: Optional[tuple] = None) -> np.ndarray:
+    """RoPE inverse frequencies (fp64), with the checkpoint's ``rope_scaling``:
+    "linear" divides every frequency by the factor (positions / factor);
+    "llama3" divides the low frequencies (wavelength > original context /
+    low_freq_factor) by the factor, keeps the high ones (wavelength < original
+    context / high_freq_factor) and interpolates linearly in
+    original_context / wavelength between them."""
     inv = theta ** (-np.arange(0, hd, 2, dtype=np.float64) / hd)
+    if scaling is None:
+        return inv
+    if scaling[0] == "linear":
+        return inv / float(scaling[1])
+    if scaling[0] == "llama3":
+        _, factor, lo, hi, ctx = scaling
+        wavelen = 2.0 * math.pi / inv
+        mix = np.clip((ctx / wavelen - lo) / (hi - lo), 0.0, 1.0)  # 0: scaled, 1: kept
+        return (1.0 - mix) * inv / factor + mix * inv
+    raise ValueError(f"unsupported rope scaling {scaling[0]!r}")
+
+
+def rope_tables(hd: int, max_seq: int, theta: float, scaling: Optional[tuple] = None):
+    inv = rope_inv_freq(hd, theta, scaling)
     ang = np.arange(max_seq, dtype=np.float64)[:, None] * inv[None, :]
     return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
 
@@ -238,14 +263,14 @@ class LlamaModel(SequenceModel):
     _pearl_device_model = True
 
     def __init__(self, cfg: LlamaConfig, weights: Dict[str, object], gemm: str = "cudacore",
-                 max_seq: int = 1024, max_tokens: int = 64, temperature: float = 1.0, bos_id: int = 1,
+                 max_seq: int = 1024, max_tokens: int = 64, temperature: float = 1.0, bos_id: Optional[int] = None,
                  latency: Optional[LatencyProfile] = None, l2_resident: bool = False, sm_count: int = 0,
                  n_slots: int = 1):
         self.device = _device.require_cuda()
         self.cfg = cfg
         self.vocab_size = cfg.vocab
         self.temperature = float(temperature)
-        self.bos_id = int(bos_id)
+        self.bos_id = int(cfg.bos_id if bos_id is None else bos_id)
         self.max_seq = int(max_seq)
         self.max_tokens = int(max_tokens)
         self.gemm = gemm
@@ -253,7 +278,7 @@ class LlamaModel(SequenceModel):
         # streamed weights packed contiguously so one L2 access-policy window covers them
         self._l2_pack = _pack_streamed(weights) if l2_resident else None
         hd = cfg.head_dim
-        cos, sin = rope_tables(hd, max_seq, cfg.rope_theta)
+        cos, sin = rope_tables(hd, max_seq, cfg.rope_theta, cfg.rope_scaling)
         self.rope_cos = torch.from_numpy(cos).to(self.device)
         self.rope_sin = torch.from_numpy(sin).to(self.device)
         # KV cache [L, slots, max_seq, KV, hd]: slot 0 serves the single-sequence
@@ -423,13 +448,25 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
     where it streams faster (tools/draft_times.py: 1.3B 1.21 vs 1.50 ms,
     8B 3.41 vs 4.51 ms per token on B200).  ``depth=(Lt, Ld)``: reduced-depth,
     full-width variant of the pair (parity tests at the BASELINE shapes)."""
+    tw, dw, tc, dc = init_pair(pair, align, depth=depth)
+    return pair_from_weights(tc, tw, dc, dw, gemm_target=gemm_target, gemm_draft=gemm_draft, max_seq=max_seq,
+                             max_tokens=max_tokens, temperature=temperature, l2_draft=l2_draft,
+                             draft_sms=draft_sms, n_slots=n_slots)
+
+
+def pair_from_weights(tc: LlamaConfig, tw, dc: LlamaConfig, dw, gemm_target: str = "cudacore",
+                      gemm_draft: str = "auto", max_seq: int = 1024, max_tokens: int = 64,
+                      temperature: float = 1.0, l2_draft: Optional[bool] = None,
+                      draft_sms: Optional[int] = None, n_slots: int = 1):
+    """(target LlamaModel, draft LlamaModel) over given weights (random-init
+    pairs and checkpoints alike); the knobs are build_pair's."""
     if l2_draft is None:
         l2_draft = os.environ.get("PEARL_L2_DRAFT", "0") == "1"
     if draft_sms is None:
         draft_sms = int(os.environ.get("PEARL_DRAFT_SMS", "0"))
     green = None
     target_sms = 0
-    if draft_sms > 0 and PRESETS[PAIRS[pair][0]].vocab > 65536:
+    if draft_sms > 0 and tc.vocab > 65536:
         # the pick / K1 kernels run 16-CTA clusters at V > 65536, which a
         # partition's GPC slices cannot host (cudaErrorInvalidClusterSize)
         import warnings
@@ -448,7 +485,6 @@ def build_pair(pair: str = "tiny", gemm_target: str = "cudacore", gemm_draft: st
             import warnings
             warnings.warn(f"green-context partition unavailable ({_lib.load().pearl_last_error().decode()}); "
                           "draft and target share all SMs")
-    tw, dw, tc, dc = init_pair(pair, align, depth=depth)
     target = LlamaModel(tc, tw, gemm=gemm_target, max_seq=max_seq,
                         max_tokens=max_tokens if gemm_target == "tcgen05" else min(max_tokens, 64),
                         temperature=temperature, sm_count=target_sms, n_slots=n_slots)

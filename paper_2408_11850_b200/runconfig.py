@@ -49,7 +49,7 @@ from typing import List, Optional, Sequence, Tuple, Union
 import numpy as np
 
 from .engines import DecodeResult, EngineConfig, write_trace_jsonl
-from .errors import InvalidAlpha
+from .errors import DeviceError, InvalidAlpha
 from .metrics import TimingParams, simulate_run, summarize_run
 
 SUMMARY_FIELDS = ["prompt", "engine", "gamma", "steps", "new_tokens", "tokens_per_step", "acceptance", "sim_time",
@@ -235,17 +235,25 @@ def build_models(cfg: RunConfig, max_seq: int = 1024):
     spec = cfg.model
     torch.cuda.set_device(spec.devices[0])
     max_tokens = 128 if spec.gemm == "tcgen05" else 64
+    eos_id = spec.eos_id
     if spec.checkpoint is not None:
         from .checkpoint import load_llama
-        tc, tw = load_llama(spec.checkpoint[0], device="cuda")
-        dc, dw = load_llama(spec.checkpoint[1], device="cuda")
+        if spec.branch_std is not None:
+            raise ConfigError("$.model.transformer.branch_std", "applies to random-init arch pairs, not checkpoints")
+        try:
+            tc, tw = load_llama(spec.checkpoint[0], device="cuda")
+            dc, dw = load_llama(spec.checkpoint[1], device="cuda")
+        except ValueError as exc:
+            raise ConfigError("$.model.transformer.checkpoint", str(exc)) from exc
         if tc.vocab != dc.vocab:
             raise ConfigError("$.model.transformer.checkpoint", f"vocab mismatch: target {tc.vocab}, draft {dc.vocab}")
-        target = llama.LlamaModel(tc, tw, gemm=spec.gemm, max_seq=max_seq, max_tokens=max_tokens,
-                                  temperature=spec.temperature, n_slots=cfg.batch)
-        draft = llama.LlamaModel(dc, dw, gemm="tcgen05" if dc.weight_bytes() > 1e9 else "cudacore", max_seq=max_seq,
-                                 max_tokens=max_tokens if dc.weight_bytes() > 1e9 else 64,
-                                 temperature=spec.temperature, n_slots=cfg.batch)
+        if tc.bos_id != dc.bos_id:
+            raise ConfigError("$.model.transformer.checkpoint", f"bos mismatch: target {tc.bos_id}, draft {dc.bos_id}")
+        target, draft = llama.pair_from_weights(tc, tw, dc, dw, gemm_target=spec.gemm, max_seq=max_seq,
+                                                max_tokens=max_tokens, temperature=spec.temperature,
+                                                n_slots=cfg.batch, draft_sms=spec.draft_sms or 0)
+        if eos_id is None:
+            eos_id = tc.eos_id  # config.json's eos_token_id
     else:
         align = llama.AlignSpec(seed=spec.seed, branch_std=spec.branch_std if spec.branch_std is not None
                                 else llama.PAIR_BRANCH_STD[spec.arch])
@@ -257,7 +265,7 @@ def build_models(cfg: RunConfig, max_seq: int = 1024):
     if timing is None:
         from .metrics import measured_params
         timing = measured_params(target, draft)
-    return draft, target, spec.eos_id, timing
+    return draft, target, eos_id, timing
 
 
 def load_prompts(cfg: RunConfig, vocab: Optional[int] = None) -> List[List[int]]:
@@ -349,6 +357,9 @@ def run(cfg: RunConfig, out_dir: Optional[str] = None, real_latency: bool = Fals
         if isinstance(cfg.model, TransformerSpec):
             longest = max(len(p) for p in load_prompts(cfg)) + 1  # + BOS
             max_seq = longest + cfg.max_new_tokens + 2 * max(cfg.gamma or 1, cfg.gamma_max) + 16
+            if max_seq > 4096:
+                raise ConfigError("$.prompts", f"longest prompt + max_new_tokens + draft slack needs a KV cache of "
+                                  f"{max_seq} positions; the kernels hold at most 4096")
         models = build_models(cfg, max_seq=max_seq)
     draft, target, eos_id, timing = models
     prompts = load_prompts(cfg, target.vocab_size)
@@ -403,6 +414,9 @@ def main(argv: Optional[Sequence[str]] = None) -> int:
     except OSError as exc:
         print(f"pearl-b200: {exc}", file=sys.stderr)
         return 3
+    except (DeviceError, ValueError) as exc:
+        print(f"pearl-b200: {exc}", file=sys.stderr)
+        return 2
     print(f"{s.engine}: {s.total_new_tokens} tokens over {s.n_prompts} prompts, "
           f"{s.tokens_per_step:.3f} tokens/step, sim speedup {s.sim_speedup:.3f}")
     print(f"artifacts in {args.out or cfg.out_dir}")

@@ -146,3 +146,80 @@ def test_hf_checkpoint_runs_on_the_kernels(tmp_path, gemm):
     got = m.forward_logits(toks).cpu()
     want = OracleLlama(cfg, w, device="cuda", bf16_points=True, max_seq=64, norm_fold=gemm == "tcgen05").forward(toks, 0).cpu()
     assert ((got - want).abs() <= 5e-2 + 1e-2 * want.abs()).all()
+
+
+ROPE_CASES = [
+    # DeepSeek-Coder 1.3B / 33B: linear scaling, factor 4
+    (2048, 16, 100000.0, {"type": "linear", "factor": 4.0}),
+    # Llama-3.1 8B / 70B: llama3 scaling
+    (4096, 32, 500000.0, {"rope_type": "llama3", "factor": 8.0, "low_freq_factor": 1.0, "high_freq_factor": 4.0,
+                          "original_max_position_embeddings": 8192}),
+    (8192, 64, 500000.0, {"rope_type": "llama3", "factor": 8.0, "low_freq_factor": 1.0, "high_freq_factor": 4.0,
+                          "original_max_position_embeddings": 8192}),
+]
+
+
+@pytest.mark.parametrize("d,H,theta,rs", ROPE_CASES)
+def test_rope_scaling_matches_transformers(d, H, theta, rs):
+    """config.json rope_scaling -> the kernels' RoPE tables: inverse
+    frequencies equal transformers' own rope-init functions (the convention
+    the checkpoints were trained with), and the oracle's independent
+    restatement equals both."""
+    import numpy as np
+    tr = pytest.importorskip("transformers")
+    from transformers.modeling_rope_utils import ROPE_INIT_FUNCTIONS
+    from paper_2408_11850_b200 import checkpoint, llama
+    from oracle import llama as ol
+    hf = dict(CFG, hidden_size=d, num_attention_heads=H, num_key_value_heads=H, intermediate_size=4 * d,
+              vocab_size=128, rope_theta=theta, rope_scaling=rs, max_position_embeddings=131072)
+    cfg = checkpoint.config_from_hf(hf)
+    assert cfg.rope_scaling is not None and cfg.rope_scaling[0] == rs.get("rope_type", rs.get("type"))
+    kind = cfg.rope_scaling[0]
+    tc = tr.LlamaConfig(hidden_size=d, num_attention_heads=H, rope_theta=theta, rope_scaling=dict(rs),
+                        max_position_embeddings=131072)
+    want, _ = ROPE_INIT_FUNCTIONS[kind](tc, "cpu")
+    ours = llama.rope_inv_freq(d // H, theta, cfg.rope_scaling)
+    assert np.allclose(ours, want.double().numpy(), rtol=1e-6, atol=0)
+    orc = ol._scaled_inv_freq(theta ** (-np.arange(0, d // H, 2, dtype=np.float64) / (d // H)), cfg.rope_scaling)
+    assert np.allclose(orc, ours, rtol=1e-12, atol=0)
+    cos, sin = llama.rope_tables(d // H, 64, theta, cfg.rope_scaling)
+    assert np.allclose(cos[37], np.cos(37 * ours).astype(np.float32))
+
+
+def test_rope_scaling_unsupported_types_are_rejected():
+    from paper_2408_11850_b200 import checkpoint
+    for rs in ({"type": "dynamic", "factor": 2.0}, {"rope_type": "yarn", "factor": 4.0}):
+        with pytest.raises(ValueError, match="rope_scaling"):
+            checkpoint.config_from_hf(dict(CFG, rope_scaling=rs))
+    assert checkpoint.config_from_hf(dict(CFG, rope_scaling=None)).rope_scaling is None
+    assert checkpoint.config_from_hf(dict(CFG, rope_scaling={"rope_type": "default"})).rope_scaling is None
+
+
+def test_bos_eos_and_vocab_from_config():
+    """BOS / EOS come from config.json (Llama-3: 128000 / list of EOS ids,
+    DeepSeek-Coder: 32013 / 32014); absent -> BOS 1, EOS None.  A vocab that
+    is not a multiple of 4 is rejected (16-byte aligned logits rows)."""
+    from paper_2408_11850_b200 import checkpoint
+    c = checkpoint.config_from_hf(dict(CFG, bos_token_id=128000, eos_token_id=[128001, 128008, 128009]))
+    assert (c.bos_id, c.eos_id) == (128000, 128001)
+    c = checkpoint.config_from_hf(dict(CFG, bos_token_id=32013, eos_token_id=32014))
+    assert (c.bos_id, c.eos_id) == (32013, 32014)
+    c = checkpoint.config_from_hf(dict(CFG))
+    assert (c.bos_id, c.eos_id) == (1, None)
+    with pytest.raises(ValueError, match="multiple of 4"):
+        checkpoint.config_from_hf(dict(CFG, vocab_size=32001))
+
+
+def test_lazy_shards_read_on_demand(tmp_path):
+    """load_llama packs from LazyShards: tensors are read per access, so the
+    host holds one layer at a time (70B checkpoints exceed host RAM twice)."""
+    from paper_2408_11850_b200 import checkpoint
+    t = _hf_tensors(2)
+    names = sorted(t)
+    checkpoint.write_safetensors(str(tmp_path / "a.safetensors"), {k: t[k] for k in names[:5]})
+    checkpoint.write_safetensors(str(tmp_path / "b.safetensors"), {k: t[k] for k in names[5:]})
+    lz = checkpoint.LazyShards([str(tmp_path / "a.safetensors"), str(tmp_path / "b.safetensors")])
+    assert len(lz) == len(t) and "lm_head.weight" in lz and lz.get("nope") is None
+    for k in names:
+        assert torch.equal(lz[k], t[k])
+    assert lz[names[0]].data_ptr() != lz[names[0]].data_ptr()  # nothing cached

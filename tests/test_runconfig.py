@@ -89,6 +89,11 @@ def test_exit_codes(tmp_path):
     nodir.write_text(json.dumps({"engine": "ar", "max_new_tokens": 4, "seed": 0,
                                  "model": {"synthetic": {"alpha": 0.5}}, "timing": {"t": 1, "c": 2}}))
     assert runconfig.main(["run", "--config", str(nodir)]) == 2
+    # a decode that needs more KV positions than the kernels hold is a config error, not a traceback
+    (tmp_path / "long.txt").write_text(" ".join(["5"] * 3000) + "\n")
+    big = tmp_path / "big.json"
+    big.write_text(json.dumps(_doc(max_new_tokens=2000, prompts=str(tmp_path / "long.txt"))))
+    assert runconfig.main(["run", "--config", str(big), "--out", str(tmp_path / "o")]) == 2
 
 
 @pytest.mark.gpu
@@ -170,13 +175,21 @@ def test_transformer_checkpoint_run(tmp_path):
         checkpoint.write_safetensors(str(tmp_path / name / "model.safetensors"), t)
         (tmp_path / name / "config.json").write_text(json.dumps(
             {"num_hidden_layers": layers, "hidden_size": d, "num_attention_heads": 4, "num_key_value_heads": 2,
-             "intermediate_size": F, "vocab_size": V}))
+             "intermediate_size": F, "vocab_size": V, "bos_token_id": 7, "eos_token_id": [1000, 1001],
+             "rope_scaling": {"type": "linear", "factor": 4.0}}))
     (tmp_path / "p.txt").write_text("5 17 300 9\n\n900 31 2\n")  # the empty line decodes from BOS
     doc = {"engine": "pearl", "gamma": 3, "max_new_tokens": 20, "seed": 4, "prompts": str(tmp_path / "p.txt"),
            "model": {"transformer": {"checkpoint": {"target": str(tmp_path / "target"),
                                                     "draft": str(tmp_path / "draft")}}}}
     (tmp_path / "cfg.json").write_text(json.dumps(doc))
+    # BOS / EOS / rope_scaling come from config.json
+    draft, target, eos_id, _ = runconfig.build_models(runconfig.load_run_config(str(tmp_path / "cfg.json")),
+                                                      max_seq=64)
+    assert (target.bos_id, draft.bos_id, eos_id) == (7, 7, 1000)
+    assert target.cfg.rope_scaling == ("linear", 4.0)
+    del draft, target
     assert runconfig.main(["run", "--config", str(tmp_path / "cfg.json"), "--out", str(tmp_path / "o")]) == 0
     out = (tmp_path / "o" / "outputs.txt").read_text().splitlines()
-    assert len(out) == 3 and all(len(line.split()) == 20 for line in out)
+    # 20 tokens each, or fewer ending at the checkpoint's EOS (1000)
+    assert len(out) == 3 and all(len(line.split()) == 20 or line.split()[-1] == "1000" for line in out)
     assert all(0 <= int(x) < V for line in out for x in line.split())
