@@ -40,30 +40,43 @@ def _newest_header() -> float:
     return max((os.path.getmtime(h) for h in hs), default=0.0)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), variant: str = "") -> str:
+    """Build the library; ``defines`` / ``variant`` make a diagnostic build
+    (e.g. ``-DPEARL_TIMELINE``) under build/var_<variant>/ that the package
+    loads only through PEARL_LIB_PATH."""
     nvcc = _nvcc()
-    os.makedirs(OBJ, exist_ok=True)
+    obj_dir = os.path.join(REPO, "build", f"var_{variant}") if variant else OBJ
+    lib = os.path.join(obj_dir, f"libpearl_{variant}.so") if variant else LIB
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     hdr_t = _newest_header()
     objs = []
     for src in srcs:
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
         objs.append(obj)
         if (not force and os.path.exists(obj)
                 and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t)):
             continue
-        cmd = [nvcc, *NVFLAGS, "-c", src, "-o", obj]
+        cmd = [nvcc, *NVFLAGS, *defines, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-lcuda"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    if "--timeline" in sys.argv:  # diagnostic build for tools/timeline.py
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, defines=("-DPEARL_TIMELINE",),
+                    variant="tl"))
+    elif "--variant" in sys.argv:  # --variant NAME -DX=Y ...: A/B builds loaded via PEARL_LIB_PATH
+        i = sys.argv.index("--variant")
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv,
+                    defines=tuple(a for a in sys.argv[i + 2:] if a.startswith("-D")), variant=sys.argv[i + 1]))
+    else:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "attention_core.cuh"
+#include "tc_common.cuh"
 #include "common.h"
 
 namespace pearl {
@@ -16,88 +18,31 @@ using bf16 = __nv_bfloat16;
 
 namespace {
 
-constexpr int kWarps = kAttnThreads / 32;
-
-
-
-__device__ __forceinline__ int tok_position(const AttnArgs& a, int p0, int t) {
-  return a.tok_pos ? a.tok_pos[t] : p0 + t;
-}
+using namespace attn_core;
 
 template <int HD>
 struct AttnSmem {
+  // warp states + weights, kAttnLCS logical folded states (at most), fold area
   static constexpr size_t kBytes =
-      (static_cast<size_t>(kWarps + 1) * kAttnMaxRb * (HD + 2) + kAttnMaxRb * kWarps +
-       kAttnMaxRb * kAttnCluster + kAttnMaxRb) * 4 + 64;
+      static_cast<size_t>(Smem<HD>::kWarpFloats + kAttnLCS * Smem<HD>::kStateFloats + Smem<HD>::kFoldFloats) * 4 + 64;
 };
-
-__device__ __forceinline__ uint32_t word(const uint4& u, int w) {
-  return w == 0 ? u.x : (w == 1 ? u.y : (w == 2 ? u.z : u.w));
-}
-
-__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
-                                         uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ uint32_t trans8x8(uint32_t x) {
-  uint32_t y;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<const uint32_t*>(&v);
-}
-
-// Register layout of a warp's 32-position segment (lane = 4 n + q):
-//   kb[nt][j] = K[P0 + 8 nt + n][32 j + 8 q .. +7]  (16 bytes)
-//   vb[i][j]  = V[P0 + 8 i  + n][32 j + 8 q .. +7]
-// The q.k contraction runs over a PERMUTED head-dim order -- for k-step
-// 2j + h the fragment's logical k = 2q + {0,1} / 2q + 8 + {0,1} is the
-// physical dim 32 j + 8 q + 4 h + {0,1} / {2,3} -- applied identically to Q
-// and K, so every fragment is one 16-byte load.  p.v's output dims are
-// permuted the same way (logical tile c = 4 j + w, pair 2q + e <-> physical
-// 32 j + 8 q + 2 w + e), and V's 8x8 blocks are transposed in registers
-// (movmatrix) into the B-fragment layout.
-template <int HD>
-__device__ __forceinline__ void load_kv(const bf16* kc, const bf16* vc, size_t kvs, int P0, int lane, int lo, int hi,
-                                        uint4 (*kb)[HD / 32], uint4 (*vb)[HD / 32]) {
-  constexpr int J = HD / 32;
-  const int n = lane >> 2, q = lane & 3;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int P = P0 + 8 * i + n;
-    if (P >= lo && P <= hi) {
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        kb[i][j] = *reinterpret_cast<const uint4*>(kc + static_cast<size_t>(P) * kvs + 32 * j + 8 * q);
-        vb[i][j] = *reinterpret_cast<const uint4*>(vc + static_cast<size_t>(P) * kvs + 32 * j + 8 * q);
-      }
-    }
-  }
-}
 
 template <int HD, int MINB>
 __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
   constexpr int J = HD / 32;    // 32-dim blocks
-  constexpr int KS = HD / 16;   // q.k k-steps
-  constexpr int NO = HD / 8;    // p.v output tiles
   constexpr int RS = HD + 2;    // state row: o[HD], m, l
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* st = reinterpret_cast<float*>(smem_raw);          // [kWarps][kAttnMaxRb][RS] warp states
-  float* cs = st + kWarps * kAttnMaxRb * RS;               // [kAttnMaxRb][RS] this CTA's folded state
-  float* wgt = cs + kAttnMaxRb * RS;                       // fold weights / sums
+  float* wgt = st + kWarps * kAttnMaxRb * RS;              // [kAttnMaxRb][kWarps] warp weights
+  float* cs = wgt + kAttnMaxRb * kWarps;                   // [per][kAttnMaxRb][RS] logical CTA states
+  float* cw = cs + kAttnLCS * kAttnMaxRb * RS;             // [R][kAttnCluster] fold weights, then [R] sums
   cg::cluster_group cluster = cg::this_cluster();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = lane >> 2, q = lane & 3;
+  if (threadIdx.x == 0) PEARL_TL(a.tl, 0);
   const int crank = static_cast<int>(cluster.block_rank());
-  const int CS = static_cast<int>(cluster.num_blocks());  // CTAs per (row block, KV head)
+  const int CS = static_cast<int>(cluster.num_blocks());  // physical CTAs per (row block, KV head)
+  const int per = kAttnLCS / CS;                          // logical CTAs per physical CTA
   const int g = a.H / a.KV;
   const int tpb = a.tpb;  // tokens per row block (tpb * g <= 16 rows)
   const bool seq_mode = a.tok_pos == nullptr;
@@ -146,8 +91,9 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
   const size_t so = a.tok_slot ? static_cast<size_t>(a.tok_slot[t0]) * static_cast<size_t>(a.slot_stride) : 0;
   const bf16* kc = a.kc + so + static_cast<size_t>(kvh) * HD;
   const bf16* vc = a.vc + so + static_cast<size_t>(kvh) * HD;
-  // segment js of this warp: 32 positions at 32 ((js CS + crank) 4 + warp)
-  auto seg_p0 = [&](int js) { return 32 * ((js * CS + crank) * kWarps + warp); };
+  // segment js of this warp in logical CTA lc: 32 positions at 32 ((js kAttnLCS + lc) 4 + warp)
+  auto seg_p0 = [&](int js, int lc) { return 32 * ((js * kAttnLCS + lc) * kWarps + warp); };
+  const int lc0 = crank * per;  // this CTA's first logical CTA
 
   uint4 kb[4][J], vb[4][J];
 #pragma unroll
@@ -156,10 +102,10 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
     for (int j = 0; j < J; ++j) kb[i][j] = vb[i][j] = make_uint4(0, 0, 0, 0);
   const int old_hi = (seq_mode && first) ? min(p0, pmax + 1) - 1 : -1;  // last position loadable before the wait
   if (first) {
-    if (seg_p0(0) <= pmax) load_kv<HD>(kc, vc, kvs, seg_p0(0), lane, 0, old_hi, kb, vb);
-    // later segments' old positions: warm L2 while the QKV GEMM drains
-    for (int js = 1; js < a.spw; ++js) {
-      const int P = seg_p0(js) + lane;
+    if (seg_p0(0, lc0) <= pmax) load_kv<HD>(kc, vc, kvs, seg_p0(0, lc0), lane, 0, old_hi, kb, vb);
+    // the other segments' old positions: warm L2 while the QKV GEMM drains
+    for (int x = 1; x < a.spw * per; ++x) {
+      const int P = seg_p0(x / per, lc0 + x % per) + lane;
       if (P <= old_hi) {
         const bf16* kr = kc + static_cast<size_t>(P) * kvs;
         const bf16* vr = vc + static_cast<size_t>(P) * kvs;
@@ -172,174 +118,36 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x == 0) PEARL_TL(a.tl, 1);
   }
 
-  // query rows lo = n, hi = n + 8 of the 16-row tile (rows >= R are zero)
-  uint4 qa[2][J];
-  int prow[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int rr = n + 8 * h, r = r0 + rr;
-    prow[h] = rr < R ? tok_position(a, p0, r / g) : -1;
-#pragma unroll
-    for (int j = 0; j < J; ++j) qa[h][j] = make_uint4(0, 0, 0, 0);
-    if (rr < R && seg_p0(0) <= pmax) {
-      const bf16* qr = a.q + (static_cast<size_t>(r / g) * a.H + kvh * g + r % g) * HD;
-#pragma unroll
-      for (int j = 0; j < J; ++j) qa[h][j] = *reinterpret_cast<const uint4*>(qr + 32 * j + 8 * q);
-    }
-  }
-  // this warp's running state for rows lo / hi: max, sum, o (NO tiles x 4)
-  float mrun[2] = {-INFINITY, -INFINITY}, lrun[2] = {0.f, 0.f};
-  float o[NO][4];
-#pragma unroll
-  for (int c = 0; c < NO; ++c) o[c][0] = o[c][1] = o[c][2] = o[c][3] = 0.f;
-  // the warp's segments in js order: a row's own positions decide what
-  // contributes, and segments past a row's position are exact no-ops for it
-  // (corr = exp(0) = 1, p = 0), so the fold never depends on the other rows
-  for (int js = 0; js < a.spw; ++js) {
-    const int P0 = seg_p0(js);
-    if (P0 > pmax) break;
-    if (js > 0) {
+  // this CTA's logical CTAs one after another: warp passes, then the fold of
+  // the 4 warp states into the logical CTA's state
+  for (int l = 0; l < per; ++l) {
+    if (l > 0) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < J; ++j) kb[i][j] = vb[i][j] = make_uint4(0, 0, 0, 0);
     }
-    load_kv<HD>(kc, vc, kvs, P0, lane, js == 0 ? old_hi + 1 : 0, pmax, kb, vb);
-    // ---- s = q . k (16 rows x 32 positions), fp32 accumulate
-    float sc[4][4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < KS; ++kk) {
-        const int j = kk >> 1, h = kk & 1;
-        mma_bf16(sc[nt], word(qa[0][j], 2 * h), word(qa[1][j], 2 * h), word(qa[0][j], 2 * h + 1),
-                 word(qa[1][j], 2 * h + 1), word(kb[nt][j], 2 * h), word(kb[nt][j], 2 * h + 1));
-      }
-    }
-    // ---- online softmax per row (lo: sc[.][0..1], hi: sc[.][2..3]) over
-    // positions P0 + 8 nt + 2 q + e; p rounded to bf16 (the p.v operand), l
-    // summed from the rounded values in a fixed (nt, e) order, then the quad
-    uint32_t pp[4][2];
-    float corr[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float m = -INFINITY;
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int P = P0 + 8 * nt + 2 * q + e;
-          sc[nt][2 * h + e] = P <= prow[h] ? sc[nt][2 * h + e] * a.scale : -INFINITY;
-          m = fmaxf(m, sc[nt][2 * h + e]);
-        }
-      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-      const float mn = fmaxf(mrun[h], m);
-      corr[h] = mrun[h] == -INFINITY ? 0.f : expf(mrun[h] - mn);
-      float l = 0.f;
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const float x0 = sc[nt][2 * h] == -INFINITY ? 0.f : expf(sc[nt][2 * h] - mn);
-        const float x1 = sc[nt][2 * h + 1] == -INFINITY ? 0.f : expf(sc[nt][2 * h + 1] - mn);
-        pp[nt][h] = pack_bf16(x0, x1);
-        const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pp[nt][h]);
-        l += __low2float(pb);
-        l += __high2float(pb);
-      }
-      l += __shfl_xor_sync(0xffffffffu, l, 1);
-      l += __shfl_xor_sync(0xffffffffu, l, 2);
-      lrun[h] = fmaf(lrun[h], corr[h], l);
-      mrun[h] = mn;
-    }
-    // ---- o = corr * o + p . v: k = 32 positions (2 steps), n = HD dims
-#pragma unroll
-    for (int c = 0; c < NO; ++c) {
-      const int j = c >> 2, w = c & 3;
-      float oc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int s2 = 0; s2 < 2; ++s2)
-        mma_bf16(oc, pp[2 * s2][0], pp[2 * s2][1], pp[2 * s2 + 1][0], pp[2 * s2 + 1][1],
-                 trans8x8(word(vb[2 * s2][j], w)), trans8x8(word(vb[2 * s2 + 1][j], w)));
-      o[c][0] = fmaf(o[c][0], corr[0], oc[0]);
-      o[c][1] = fmaf(o[c][1], corr[0], oc[1]);
-      o[c][2] = fmaf(o[c][2], corr[1], oc[2]);
-      o[c][3] = fmaf(o[c][3], corr[1], oc[3]);
-    }
+    warp_pass<HD>(a, kc, vc, kvs, p0, r0, R, g, kvh, pmax, kAttnLCS, lc0 + l, warp, lane, a.spw,
+                  l == 0 ? old_hi : -1, kb, vb, st + warp * kAttnMaxRb * RS);
+    __syncthreads();
+    cta_fold<HD>(st, cs + l * kAttnMaxRb * RS, wgt, R, threadIdx.x, kAttnThreads, [] { __syncthreads(); });
+    __syncthreads();
   }
-  // warp state -> smem: logical dims 2q + {0,1} of tile c = physical 32 j + 8 q + 2 w + {0,1}
-  float* sw = st + warp * kAttnMaxRb * RS;
-#pragma unroll
-  for (int c = 0; c < NO; ++c) {
-    const int d = 32 * (c >> 2) + 8 * q + 2 * (c & 3);
-    *reinterpret_cast<float2*>(sw + n * RS + d) = make_float2(o[c][0], o[c][1]);
-    *reinterpret_cast<float2*>(sw + (n + 8) * RS + d) = make_float2(o[c][2], o[c][3]);
-  }
-  if (q == 0) {
-    sw[n * RS + HD] = mrun[0];
-    sw[n * RS + HD + 1] = lrun[0];
-    sw[(n + 8) * RS + HD] = mrun[1];
-    sw[(n + 8) * RS + HD + 1] = lrun[1];
-  }
+  // fold of the kAttnLCS logical states in order (DSMEM across the cluster);
+  // logical CTA lc produces head dims [lc HD / kAttnLCS, (lc + 1) HD / kAttnLCS)
+  if (CS > 1) cluster.sync();
+  auto peer = [&](int c) -> const float* {
+    return cluster.map_shared_rank(cs + (c % per) * kAttnMaxRb * RS, c / per);
+  };
+  cluster_weights<HD>(peer, kAttnLCS, R, cw, threadIdx.x);
   __syncthreads();
-  // CTA fold over its warps in warp order (weights exp(m_w - max), 0 = empty)
-  if (threadIdx.x < R * kWarps) {
-    const int rr = threadIdx.x / kWarps, w = threadIdx.x % kWarps;
-    float mx = -INFINITY;
-#pragma unroll
-    for (int x = 0; x < kWarps; ++x) mx = fmaxf(mx, st[(x * kAttnMaxRb + rr) * RS + HD]);
-    const float mw = st[(w * kAttnMaxRb + rr) * RS + HD];
-    wgt[rr * kWarps + w] = mw == -INFINITY ? 0.f : expf(mw - mx);
-    if (w == 0) cs[rr * RS + HD] = mx;
-  }
+  cluster_sums<HD>(peer, kAttnLCS, R, cw, threadIdx.x);
   __syncthreads();
-  for (int i = threadIdx.x; i < R * (HD + 1); i += kAttnThreads) {
-    const int rr = i / (HD + 1), d = i % (HD + 1);  // d == HD: the row's l
-    const int col = d < HD ? d : HD + 1;
-    float acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const float wt = wgt[rr * kWarps + w];
-      if (wt != 0.f) acc = fmaf(wt, st[(w * kAttnMaxRb + rr) * RS + col], acc);
-    }
-    cs[rr * RS + col] = acc;
-  }
-  // cluster fold over the CTAs in rank order (DSMEM); CTA `crank` produces
-  // head dims [crank * HD / CS, (crank + 1) * HD / CS) of every row.  A
-  // single-CTA "cluster" (CS = 1) folds its own state the same way.
-  if (CS > 1) cluster.sync(); else __syncthreads();
-  const int DC = HD / CS;  // dims per CTA
-  float* cw = wgt + kAttnMaxRb * kWarps;  // [R][kAttnCluster] weights, then [R] sums
-  if (threadIdx.x < R * CS) {
-    const int rr = threadIdx.x / CS, c = threadIdx.x % CS;
-    float mx = -INFINITY;
-    for (int x = 0; x < CS; ++x) mx = fmaxf(mx, cluster.map_shared_rank(cs, x)[rr * RS + HD]);
-    const float mc = cluster.map_shared_rank(cs, c)[rr * RS + HD];
-    cw[rr * kAttnCluster + c] = mc == -INFINITY ? 0.f : expf(mc - mx);
-  }
-  __syncthreads();
-  if (threadIdx.x < R) {
-    const int rr = threadIdx.x;
-    float L = 0.f;
-    for (int c = 0; c < CS; ++c) {
-      const float wt = cw[rr * kAttnCluster + c];
-      if (wt != 0.f) L = fmaf(wt, cluster.map_shared_rank(cs, c)[rr * RS + HD + 1], L);
-    }
-    cw[kAttnMaxRb * kAttnCluster + rr] = L;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < R * DC; i += kAttnThreads) {
-    const int rr = i / DC, d = crank * DC + i % DC;
-    float O = 0.f;
-    for (int c = 0; c < CS; ++c) {
-      const float wt = cw[rr * kAttnCluster + c];
-      if (wt != 0.f) O = fmaf(wt, cluster.map_shared_rank(cs, c)[rr * RS + d], O);
-    }
-    const int r = r0 + rr, t = r / g, h = kvh * g + r % g;
-    a.o[(static_cast<size_t>(t) * a.H + h) * HD + d] = __float2bfloat16(O / cw[kAttnMaxRb * kAttnCluster + rr]);
-  }
+  for (int l = 0; l < per; ++l)
+    cluster_out<HD>(a, peer, kAttnLCS, lc0 + l, R, r0, g, kvh, cw, threadIdx.x, kAttnThreads);
   if (CS > 1) cluster.sync();  // the peers' states stay alive until every CTA has read them
   else __syncthreads();         // smem reuse by the next item
   first = false;
@@ -348,6 +156,7 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
+  if (threadIdx.x == 0) PEARL_TL(a.tl, 4);
 }
 
 std::once_flag g_once;
@@ -380,7 +189,7 @@ int attn_cluster_size(bool slot_mode) {
   static const int cs = [] {
     const char* v = std::getenv("PEARL_ATTN_CLUSTER");
     const int x = v ? std::atoi(v) : kAttnClusterDefault;
-    return (x == 1 || x == 2 || x == 4 || x == 8) ? x : kAttnClusterDefault;
+    return (x == 1 || x == 2 || x == 4) ? x : kAttnClusterDefault;
   }();
   return cs;
 }
@@ -397,10 +206,10 @@ void attn_plan(const AttnShape& s, int* tpb, int* spw, int* grid) {
   const int g = s.H / s.KV;
   // tokens per row block: one 16-row MMA tile of (token, query head) rows
   *tpb = std::max(1, kAttnMaxRb / g);
-  // segments per warp: the cluster's CS CTAs x 4 warps cover the whole
-  // cache in spw rounds of 128 CS positions (a function of max_seq only)
+  // segments per warp: the kAttnLCS logical CTAs x 4 warps cover the whole
+  // cache in spw rounds of 512 positions (a function of max_seq only)
   const int CS = attn_cluster_size(s.slot_mode);
-  *spw = (s.max_seq + 128 * CS - 1) / (128 * CS);
+  *spw = (s.max_seq + 128 * kAttnLCS - 1) / (128 * kAttnLCS);
   // row blocks: sequence mode ceil(M / tpb); slot mode at most one per token
   // run chunk, bounded by M.  One cluster per (block, KV head) item: items
   // past the device-side block count exit at once
@@ -408,7 +217,11 @@ void attn_plan(const AttnShape& s, int* tpb, int* spw, int* grid) {
   *grid = nblk_max * s.KV * CS;
 }
 
-int attn_launch(const AttnArgs& a, int hd, int grid, cudaStream_t st) {
+int attn_launch(const AttnArgs& a_in, int hd, int grid, cudaStream_t st) {
+  AttnArgs a = a_in;
+#ifdef PEARL_TIMELINE
+  a.tl = timeline_next(1);
+#endif
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kAttnThreads);

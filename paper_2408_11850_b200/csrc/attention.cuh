@@ -38,8 +38,15 @@
 namespace pearl {
 
 constexpr int kAttnThreads = 128;   // 4 warps
-constexpr int kAttnCluster = 8;     // largest cluster (CTAs per (row block, KV head))
-constexpr int kAttnClusterDefault = 4;  // measured best on B200 (7B M=4: 1 -> 3.09, 2 -> 2.98, 4 -> 2.97 ms)
+// The fold is defined over kAttnLCS LOGICAL CTAs x 4 warps per (row block,
+// KV head) -- the arithmetic of every output row -- whatever the physical
+// cluster: a cluster of CS CTAs (1, 2 or 4) runs kAttnLCS / CS logical CTAs
+// per physical CTA one after another, and the fold reads logical state c
+// from physical rank c / (kAttnLCS / CS).  Sequence mode (CS = 4) and slot
+// mode (CS = 1) therefore give bitwise the same rows (batched == single).
+constexpr int kAttnLCS = 4;
+constexpr int kAttnCluster = kAttnLCS;  // fold width (logical CTAs)
+constexpr int kAttnClusterDefault = 4;  // physical, sequence mode: measured best on B200 (7B M=4: 1 -> 3.09, 2 -> 2.98, 4 -> 2.97 ms)
 constexpr int kAttnMaxRb = 16;      // rows per block (one m16n8k16 row tile)
 constexpr int kAttnMaxTok = 128;    // tokens per launch (a model's max_tokens)
 
@@ -57,7 +64,8 @@ struct AttnArgs {
   float scale;
   int tpb;                  // tokens per row block (rows t * g + j, <= 16); slot mode
                             // blocks never straddle a run of same-slot tokens
-  int spw;                  // segments per warp (rounds of 128 x cluster-size positions)
+  int spw;                  // segments per warp (rounds of 512 positions)
+  unsigned long long* tl;   // PEARL_TIMELINE builds: this launch's stamps
 };
 
 // Host: plan (rb, nrb) for a window of M tokens, launch on stream st.
@@ -66,7 +74,7 @@ struct AttnShape {
   bool slot_mode;
 };
 void attn_plan(const AttnShape& s, int* tpb, int* spw, int* grid);
-int attn_cluster_size(bool slot_mode);  // CTAs per cluster (PEARL_ATTN_CLUSTER: 1, 2, 4, 8)
+int attn_cluster_size(bool slot_mode);  // physical CTAs per cluster (PEARL_ATTN_CLUSTER: 1, 2, 4)
 int attn_launch(const AttnArgs& a, int hd, int grid, cudaStream_t st);
 int attn_init();  // one-time kernel attributes
 

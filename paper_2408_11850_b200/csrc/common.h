@@ -35,6 +35,27 @@ bool pdl_enabled();
     }                                       \
   } while (0)
 
+// Diagnostic builds only (-DPEARL_TIMELINE, tools/timeline.py): per-CTA
+// globaltimer stamps of every GEMM / attention launch, kTlSlots u64 per CTA.
+#ifdef PEARL_TIMELINE
+constexpr int kTlSlots = 16;
+constexpr int kTlCtas = 160;
+struct Timeline {
+  unsigned long long* buf = nullptr;  // [max_launches][kTlCtas][kTlSlots]
+  int max_launches = 0;
+  int seq = 0;                        // next launch index (host)
+};
+Timeline& timeline();
+// device-side stamp target of one launch (nullptr when disabled / full)
+inline unsigned long long* timeline_next(int kind) {
+  Timeline& t = timeline();
+  if (!t.buf || t.seq >= t.max_launches) return nullptr;
+  unsigned long long* p = t.buf + static_cast<size_t>(t.seq++) * kTlCtas * kTlSlots;
+  (void)kind;
+  return p;
+}
+#endif
+
 // Pairwise-sum plan for a vocabulary size (plan.cpp).
 struct VocabPlan {
   int V = 0;

@@ -44,6 +44,7 @@ struct TcArgs {
   EpiArgs e;
   float* partials;
   int* flags;
+  unsigned long long* tl;  // PEARL_TIMELINE builds: this launch's stamps
 };
 
 // W tile (tile, kb): row-major [N, K] -> box at (k = 64 kb, row = 128 tile);
@@ -76,6 +77,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) PEARL_TL(a.tl, 0);
   const long long r0 = static_cast<long long>(blockIdx.x) * a.T / a.G;
   const long long r1 = static_cast<long long>(blockIdx.x + 1) * a.T / a.G;
   const int total = static_cast<int>(r1 - r0);
@@ -124,6 +126,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         if (++kb == a.KB) { kb = 0; ++tile; }
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      PEARL_TL(a.tl, 1);
       if (blockIdx.x == 0 && a.e.adv_pos != nullptr) *a.e.adv_pos += a.e.adv_n;
       int kx = kb_start;
       for (int it = 0; it < npre; ++it) {
@@ -158,6 +161,9 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
           mbar_wait(&full[s], (it / stages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           unsigned char* st = smem + s * stage_bytes;
+#ifdef PEARL_TIMELINE
+          if (it == 0) PEARL_TL(a.tl, 2);
+#endif
           const uint64_t adesc = umma_desc_sw128(st);
           // all NT token tiles in ONE MMA of N = 16 NT columns (the tiles are
           // contiguous rows of one SW128 operand); per-column arithmetic is the
@@ -171,6 +177,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         }
         umma_commit(&acc_full[b]);
       }
+      PEARL_TL(a.tl, 3);
     }
   } else {
     // ---- epilogue warps 2..5
@@ -252,6 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 64) PEARL_TL(a.tl, 4);
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
 }
 
@@ -437,6 +445,11 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.e = e;
   a.partials = ctx.partials;
   a.flags = ctx.tile_flags;
+#ifdef PEARL_TIMELINE
+  a.tl = timeline_next(0);
+#else
+  a.tl = nullptr;
+#endif
   if (static_cast<size_t>(tiles) * a.seg_max * kTileN * kMaxTokTiles * kTokTile > ctx.partial_floats ||
       tiles > ctx.n_flags) {
     set_error("tc_gemm: shape exceeds the planned split-K workspace");

@@ -157,6 +157,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ const double* cluster_gather_d(ClusterCtx& cc, Scratch& s, const double* v, int nv) {
   if (threadIdx.x == 0)
     for (int k = 0; k < nv; ++k) s.xchg[cc.parity][k] = v[k];
+  __syncwarp();  // reconverge warp 0 before the (cluster) barrier
   if (cc.size == 1) {
     __syncthreads();
     if (threadIdx.x < nv) s.gath_d[threadIdx.x] = s.xchg[cc.parity][threadIdx.x];
@@ -165,6 +166,7 @@ __device__ __forceinline__ const double* cluster_gather_d(ClusterCtx& cc, Scratc
     if (threadIdx.x < cc.size * 4 && (threadIdx.x & 3) < nv)
       s.gath_d[threadIdx.x] = cg::this_cluster().map_shared_rank(&s.xchg[cc.parity][0], threadIdx.x >> 2)[threadIdx.x & 3];
   }
+  __syncwarp();
   __syncthreads();
   cc.parity ^= 1;
   return s.gath_d;
@@ -173,6 +175,7 @@ __device__ __forceinline__ const double* cluster_gather_d(ClusterCtx& cc, Scratc
 __device__ __forceinline__ const int* cluster_gather_i(ClusterCtx& cc, Scratch& s, const int* v, int nv) {
   if (threadIdx.x == 0)
     for (int k = 0; k < nv; ++k) s.xchg_i[cc.parity][k] = v[k];
+  __syncwarp();  // reconverge warp 0 before the (cluster) barrier
   if (cc.size == 1) {
     __syncthreads();
     if (threadIdx.x < nv) s.gath_i[threadIdx.x] = s.xchg_i[cc.parity][threadIdx.x];
@@ -181,6 +184,7 @@ __device__ __forceinline__ const int* cluster_gather_i(ClusterCtx& cc, Scratch& 
     if (threadIdx.x < cc.size * 4 && (threadIdx.x & 3) < nv)
       s.gath_i[threadIdx.x] = cg::this_cluster().map_shared_rank(&s.xchg_i[cc.parity][0], threadIdx.x >> 2)[threadIdx.x & 3];
   }
+  __syncwarp();
   __syncthreads();
   cc.parity ^= 1;
   return s.gath_i;
@@ -440,7 +444,10 @@ __device__ int cluster_search(ClusterCtx& cc, Scratch& s, const int* plan, int V
   int ans = -1;
   for (int r = 0; r < cc.size; ++r) {
     double v2[2] = {0.0, 0.0};
-    if (cc.rank == r && threadIdx.x == 0) {
+    // the whole of warp 0 runs the replay in lockstep (every lane the same
+    // values; lane 0's are published), so no warp reaches the following
+    // barriers partially diverged
+    if (cc.rank == r && threadIdx.x < 32) {
       double cc_ = carry;
       int an = ans;
       for (int i = lo; i < hi && an < 0; ++i) {
@@ -450,6 +457,7 @@ __device__ int cluster_search(ClusterCtx& cc, Scratch& s, const int* plan, int V
       v2[0] = cc_;
       v2[1] = static_cast<double>(an);
     }
+    __syncwarp();
     const double* got = cluster_gather_d(cc, s, v2, 2);
     carry = got[4 * r];
     if (ans < 0) ans = static_cast<int>(got[4 * r + 1]);

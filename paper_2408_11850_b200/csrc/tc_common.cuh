@@ -28,9 +28,16 @@ constexpr int kAccs = 4;  // TMEM accumulators (x NT*16 fp32 columns) in flight
 // under programmatic dependent launch): 7B forward M=4 3.43 -> 3.31 ms,
 // M=16 4.0 -> 3.77 ms, M=24 5.15 -> 4.35 ms (B200, graph replay).  A
 // 200 KB / 12-stage ring measured no better.
+// Diagnostic builds may override the ring size / co-residency (A/B probes).
+#ifndef PEARL_RING_KB
+#define PEARL_RING_KB 144
+#endif
+#ifndef PEARL_GEMM_MINB
+#define PEARL_GEMM_MINB 1
+#endif
 template <int NT>
 struct TcCfg {
-  static constexpr int kRing = 144 * 1024;
+  static constexpr int kRing = PEARL_RING_KB * 1024;
   static constexpr int kStageBytes = kWBytes + NT * kXBytes;
   static constexpr int kStages = (kRing / kStageBytes) < kMaxStages ? (kRing / kStageBytes) : kMaxStages;
   // staged tile, token-major: E[t * kEStride + row] (+4 pad keeps rows 16-byte aligned)
@@ -39,7 +46,7 @@ struct TcCfg {
   static constexpr int kCols = kAccs * NT * 16;
   static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + kEBytes + 512;
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocks = PEARL_GEMM_MINB;
 };
 
 
@@ -159,5 +166,21 @@ __device__ __forceinline__ Unit unit_at(const A& a, long long x, long long r1) {
   return u;
 }
 
+
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef PEARL_TIMELINE
+#define PEARL_TL(buf, slot)                                                                        \
+  do {                                                                                             \
+    if ((buf) != nullptr && blockIdx.x < 160) (buf)[blockIdx.x * 16 + (slot)] = ::pearl::tl_now(); \
+  } while (0)
+#else
+#define PEARL_TL(buf, slot) \
+  do {                      \
+  } while (0)
+#endif
 
 }  // namespace pearl

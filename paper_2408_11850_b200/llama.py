@@ -492,10 +492,11 @@ def pair_from_weights(tc: LlamaConfig, tw, dc: LlamaConfig, dw, gemm_target: str
         gemm_draft = "tcgen05" if dc.weight_bytes() > 1e9 else "cudacore"
     # the CUDA-core engine's fused-norm prologue takes <= 64 tokens per pass
     draft_tokens = max_tokens if gemm_draft == "tcgen05" else min(max_tokens, 64)
-    # a tcgen05 draft on its own partition sizes its persistent grids to it
+    # a draft on its own partition sizes its persistent grids to it (tcgen05
+    # stream-K grids; the CUDA-core model's single-token persistent forward,
+    # whose grid barrier needs every CTA co-resident)
     draft = LlamaModel(dc, dw, gemm=gemm_draft, max_seq=max_seq, max_tokens=draft_tokens, temperature=temperature,
-                       l2_resident=l2_draft, n_slots=n_slots,
-                       sm_count=green[2] if green is not None and gemm_draft == "tcgen05" else 0)
+                       l2_resident=l2_draft, n_slots=n_slots, sm_count=green[2] if green is not None else 0)
     if green is not None:
         target.green_partition = green  # (draft stream, target stream, draft SMs, target SMs)
     return target, draft

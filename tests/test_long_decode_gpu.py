@@ -4,8 +4,8 @@ The device engines consume the reference's RandomStream uniforms
 (core.py:135-179) from 4096-entry device tables with device cursors, and the
 host refills a table (``consume`` + ``peek``) when a cursor nears its end
 (fastpath._Tables.advance, batched._BatchRuntime.load_table).  A decode that
-draws more than 4096 uniforms from one stream must still reproduce the
-reference engine draw for draw.  Here the draft stream of a gamma = 32 PEARL /
+draws more uniforms than a table holds must still reproduce the reference
+engine draw for draw.  Here the draft stream of a gamma = 32 PEARL /
 SD decode crosses the table end several times, with the context running up
 to within a few positions of max_seq = 4096 (the kernels' limit).
 """
@@ -20,17 +20,25 @@ torch = pytest.importorskip("torch")
 GAMMA = 24
 PROMPT = 3600
 NEW = 400
+TABLE = 128
 
 
 @pytest.fixture(scope="module")
 def pair():
+    """Tiny pair whose runtimes hold 128-entry uniform tables instead of
+    4096 (fastpath.U_TABLE / batched.U_TABLE, patched before the runtimes
+    exist), so a few hundred steps cross the table end many times and every
+    refill (consume + peek + cursor reset) is exercised; the refill code and
+    the kernels' table/cursor arguments are the production ones."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    from paper_2408_11850_b200 import llama
-    # weakly aligned pair (branch std 0.02): short accepted runs, many steps,
-    # so the draft stream draws gamma uniforms per step for hundreds of steps
-    return llama.build_pair("tiny", gemm_target="tcgen05", max_seq=4096, max_tokens=64, n_slots=2,
-                            align=llama.AlignSpec(branch_std=0.02))
+    from paper_2408_11850_b200 import batched, fastpath, llama
+    mp = pytest.MonkeyPatch()
+    mp.setattr(fastpath, "U_TABLE", TABLE)
+    mp.setattr(batched, "U_TABLE", TABLE)
+    yield llama.build_pair("tiny", gemm_target="tcgen05", max_seq=4096, max_tokens=64, n_slots=2,
+                           align=llama.AlignSpec(branch_std=0.02))
+    mp.undo()
 
 
 def _prefix(seed):
@@ -52,7 +60,7 @@ def test_long_decode_refills_tables_and_matches_reference(pair, engine):
     cfg = pk.EngineConfig(gamma=GAMMA, max_new_tokens=NEW, seed=3)
     res = (pk.decode_pearl if engine == "pearl" else pk.decode_sd)(draft, target, prefix, cfg)
     # the draft stream alone draws gamma uniforms per step: well past one table
-    assert len(res.steps) * GAMMA > 4096, len(res.steps)
+    assert len(res.steps) * GAMMA > 3 * TABLE, len(res.steps)
     assert len(res.tokens) == NEW
     assert PROMPT + 1 + NEW + GAMMA > 4000  # the context ends near max_seq
     fn = oe.decode_pearl if engine == "pearl" else oe.decode_sd
@@ -72,6 +80,6 @@ def test_long_batched_decode_equals_single(pair):
     got = batched.decode_pearl_batch(draft, target, prompts, cfg)
     for i, p in enumerate(prompts):
         one = pk.decode_pearl(draft, target, p, replace(cfg, seed=batched.derive_seed(cfg.seed, i)))
-        assert len(one.steps) * GAMMA > 4096
+        assert len(one.steps) * GAMMA > 3 * TABLE
         assert got[i].tokens == one.tokens
         assert _strip(got[i].steps) == _strip(one.steps)

@@ -31,9 +31,8 @@ for M in Ms:
     X = torch.randn(M, max(K for _, K in shapes), device="cuda").to(torch.bfloat16)
     Y = torch.empty(M, max(N for N, _ in shapes), device="cuda")
     for name, WW, kind in (("rowmajor", Ws, 1), ("tiled", Wt, 1 | 0x100)):
-        st = torch.cuda.current_stream().cuda_stream
-
         def run():
+            st = torch.cuda.current_stream().cuda_stream
             for layer in WW:
                 for W, (N, K) in zip(layer, shapes):
                     rc = lib.pearl_gemm(kind, W.data_ptr(), X.data_ptr(), Y.data_ptr(), M, N, K, 0, st)
