@@ -35,7 +35,6 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
   float* st = reinterpret_cast<float*>(smem_raw);          // [kWarps][kAttnMaxRb][RS] warp states
   float* wgt = st + kWarps * kAttnMaxRb * RS;              // [kAttnMaxRb][kWarps] warp weights
   float* cs = wgt + kAttnMaxRb * kWarps;                   // [per][kAttnMaxRb][RS] logical CTA states
-  float* cw = cs + kAttnLCS * kAttnMaxRb * RS;             // [R][kAttnCluster] fold weights, then [R] sums
   cg::cluster_group cluster = cg::this_cluster();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -142,12 +141,8 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
   auto peer = [&](int c) -> const float* {
     return cluster.map_shared_rank(cs + (c % per) * kAttnMaxRb * RS, c / per);
   };
-  cluster_weights<HD>(peer, kAttnLCS, R, cw, threadIdx.x);
-  __syncthreads();
-  cluster_sums<HD>(peer, kAttnLCS, R, cw, threadIdx.x);
-  __syncthreads();
   for (int l = 0; l < per; ++l)
-    cluster_out<HD>(a, peer, kAttnLCS, lc0 + l, R, r0, g, kvh, cw, threadIdx.x, kAttnThreads);
+    cluster_fold_out<HD>(a, peer, kAttnLCS, lc0 + l, R, r0, g, kvh, threadIdx.x, kAttnThreads);
   if (CS > 1) cluster.sync();  // the peers' states stay alive until every CTA has read them
   else __syncthreads();         // smem reuse by the next item
   first = false;

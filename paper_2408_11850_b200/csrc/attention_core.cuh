@@ -228,6 +228,7 @@ __device__ __forceinline__ void cta_fold(const float* st, float* cs, float* wgt,
     if (w == 0) cs[rr * RS + HD] = mx;
   }
   sync();
+#pragma unroll 4
   for (int i = tid; i < R * (HD + 1); i += nthr) {
     const int rr = i / (HD + 1), d = i % (HD + 1);  // d == HD: the row's l
     const int col = d < HD ? d : HD + 1;
@@ -285,6 +286,49 @@ __device__ __forceinline__ void cluster_out(const AttnArgs& a, Peer peer, int CS
     }
     const int r = r0 + rr, t = r / g, h = kvh * g + r % g;
     a.o[(static_cast<size_t>(t) * a.H + h) * HD + d] = __float2bfloat16(O / cw[kAttnMaxRb * kAttnCluster + rr]);
+  }
+}
+
+// The three fold steps above in ONE pass: each output thread (row rr, dim d)
+// loads the CS states' m, l and o[d] together (one DSMEM / smem round trip,
+// no barriers), recomputes the row's weights and denominator in the same
+// order with the same operations, and writes o -- bitwise the same rows as
+// cluster_weights + cluster_sums + cluster_out.
+template <int HD, typename Peer>
+__device__ __forceinline__ void cluster_fold_out(const AttnArgs& a, Peer peer, int CS, int crank, int R, int r0, int g,
+                                                 int kvh, int tid, int nthr) {
+  constexpr int RS = HD + 2;
+  const int DC = HD / CS;
+#pragma unroll 4
+  for (int i = tid; i < R * DC; i += nthr) {
+    const int rr = i / DC, d = crank * DC + i % DC;
+    float m[kAttnCluster], l[kAttnCluster], o[kAttnCluster];
+#pragma unroll
+    for (int c = 0; c < kAttnCluster; ++c) {
+      if (c < CS) {
+        const float* st = peer(c) + rr * RS;
+        m[c] = st[HD];
+        l[c] = st[HD + 1];
+        o[c] = st[d];
+      }
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < kAttnCluster; ++c)
+      if (c < CS) mx = fmaxf(mx, m[c]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int c = 0; c < kAttnCluster; ++c) {
+      if (c < CS) {
+        const float wt = m[c] == -INFINITY ? 0.f : expf(m[c] - mx);
+        if (wt != 0.f) {
+          L = fmaf(wt, l[c], L);
+          O = fmaf(wt, o[c], O);
+        }
+      }
+    }
+    const int r = r0 + rr, t = r / g, h = kvh * g + r % g;
+    a.o[(static_cast<size_t>(t) * a.H + h) * HD + d] = __float2bfloat16(O / L);
   }
 }
 

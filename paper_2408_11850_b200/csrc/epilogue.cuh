@@ -162,18 +162,22 @@ __device__ __forceinline__ float4 scale4(float4 v, float r) {
 }
 
 // rs: per-token norm scales in smem (nullptr: no folded norm).
+// t_base: this call covers tokens t_base .. min(M, t_base + MAXI * 4) - 1
+// (wide windows run it in 64-token slices, bounding the registers per thread).
 template <int MAXI, bool TR = false>
 __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const float* E, int ES, int M, int N,
-                                              int et, const float* rs = nullptr) {
+                                              int et, const float* rs = nullptr, int t_base = 0) {
   constexpr int kGroups = 32;  // 128 rows / 4
-  const int nitems = kGroups * M;
+  E += static_cast<size_t>(t_base) * (TR ? ES : 1);
+  if (rs) rs += t_base;
+  const int nitems = kGroups * (M - t_base < MAXI * 4 ? M - t_base : MAXI * 4);
   switch (e.kind) {
     case EPI_STORE_F32:
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
-        float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
+        float* o = e.out_f32 + static_cast<size_t>(t_base + t) * e.ld + n0;
         float4 v = epi_rows4<TR>(E, ES, g, t);
         if (rs) v = scale4(v, rs[t]);
         if (n0 + 3 < N && (e.ld & 3) == 0) {
@@ -191,7 +195,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx < nitems && n0 + 3 < N)
-          hv[i] = *reinterpret_cast<const float4*>(e.out_f32 + static_cast<size_t>(t) * e.ld + n0);
+          hv[i] = *reinterpret_cast<const float4*>(e.out_f32 + static_cast<size_t>(t_base + t) * e.ld + n0);
       }
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
@@ -199,7 +203,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
         if (idx >= nitems) continue;  // uniform per warp: a warp's 32 lanes are one token's 32 groups
         float4 hn = make_float4(0.f, 0.f, 0.f, 0.f);
         if (n0 < N) {
-          float* o = e.out_f32 + static_cast<size_t>(t) * e.ld + n0;
+          float* o = e.out_f32 + static_cast<size_t>(t_base + t) * e.ld + n0;
           const float4 v = epi_rows4<TR>(E, ES, g, t);
           if (n0 + 3 < N) {
             hn = make_float4(hv[i].x + v.x, hv[i].y + v.y, hv[i].z + v.z, hv[i].w + v.w);
@@ -215,11 +219,11 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
             const float4 gv = __ldg(reinterpret_cast<const float4*>(e.gain + n0));  // same for every token: cached
             const __nv_bfloat162 lo = __floats2bfloat162_rn(hn.x * gv.x, hn.y * gv.y);
             const __nv_bfloat162 hi = __floats2bfloat162_rn(hn.z * gv.z, hn.w * gv.w);
-            *reinterpret_cast<uint2*>(e.x_out + static_cast<size_t>(t) * e.ld + n0) =
+            *reinterpret_cast<uint2*>(e.x_out + static_cast<size_t>(t_base + t) * e.ld + n0) =
                 make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
           }
           const float ss = tile_sumsq(hn);
-          if (g == 0) e.ss_out[static_cast<size_t>(tile) * e.ss_ld + t] = ss;
+          if (g == 0) e.ss_out[static_cast<size_t>(tile) * e.ss_ld + t_base + t] = ss;
         }
       }
       break;
@@ -231,8 +235,8 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
         if (idx >= nitems || n0 >= N) continue;
         float4 v = epi_rows4<TR>(E, ES, g, t);
         if (rs) v = scale4(v, rs[t]);
-        e.out_bf16[static_cast<size_t>(t) * e.ld + n0 / 2] = __float2bfloat16(swiglu1(v.x, v.y));
-        e.out_bf16[static_cast<size_t>(t) * e.ld + (n0 + 2) / 2] = __float2bfloat16(swiglu1(v.z, v.w));
+        e.out_bf16[static_cast<size_t>(t_base + t) * e.ld + n0 / 2] = __float2bfloat16(swiglu1(v.x, v.y));
+        e.out_bf16[static_cast<size_t>(t_base + t) * e.ld + (n0 + 2) / 2] = __float2bfloat16(swiglu1(v.z, v.w));
       }
       break;
     case EPI_QKV: {
@@ -243,7 +247,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx < nitems && n0 < e.n_q + e.n_kv) {
-          const size_t off = static_cast<size_t>(e.tok_pos ? e.tok_pos[t] : p0 + t) * half + ((n0 % e.hd) >> 1);
+          const size_t off = static_cast<size_t>(e.tok_pos ? e.tok_pos[t_base + t] : p0 + t_base + t) * half + ((n0 % e.hd) >> 1);
           cs[i] = *reinterpret_cast<const float2*>(e.cos_t + off);
           sn[i] = *reinterpret_cast<const float2*>(e.sin_t + off);
         }
@@ -252,8 +256,8 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       for (int i = 0; i < MAXI; ++i) {
         const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
-        const int p = e.tok_pos ? e.tok_pos[t] : p0 + t;
-        const size_t so = epi_slot_off(e, t);
+        const int p = e.tok_pos ? e.tok_pos[t_base + t] : p0 + t_base + t;
+        const size_t so = epi_slot_off(e, t_base + t);
         float4 v4 = epi_rows4<TR>(E, ES, g, t);
         if (rs) v4 = scale4(v4, rs[t]);
         const float v[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -261,7 +265,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
           float w[4];
           rope2(v[0], v[1], cs[i].x, sn[i].x, &w[0], &w[1]);
           rope2(v[2], v[3], cs[i].y, sn[i].y, &w[2], &w[3]);
-          bf16* dst = n0 < e.n_q ? e.out_bf16 + static_cast<size_t>(t) * e.n_q + n0
+          bf16* dst = n0 < e.n_q ? e.out_bf16 + static_cast<size_t>(t_base + t) * e.n_q + n0
                                  : e.kc + so + static_cast<size_t>(p) * e.n_kv + (n0 - e.n_q);
           for (int r = 0; r < 4; ++r) dst[r] = __float2bfloat16(w[r]);
         } else {

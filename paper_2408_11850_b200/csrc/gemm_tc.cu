@@ -202,22 +202,26 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
       const int b = ui % kAccs;
       mbar_wait(&acc_full[b], (ui / kAccs) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float v[NT * 16];
+      // the accumulator in 16-column chunks (16 registers live, not 16 NT):
+      // token-major staging of the tile (a warp's 32 rows of one token are
+      // 128 contiguous bytes) or this split's fp32 partial [t][row] (coalesced)
+      float* dst = a.partials + (static_cast<size_t>(tile) * a.seg_max + u.seg) * Mp * kTileN + row;
+#pragma unroll 1
+      for (int j = 0; j < NT; ++j) {
+        float v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * NT * kTokTile + j * kTokTile, v);
+        if (u.nseg == 1) {
 #pragma unroll
-      for (int j = 0; j < NT; ++j)
-        tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * NT * kTokTile + j * kTokTile, v + 16 * j);
+          for (int c = 0; c < 16; ++c) E[(16 * j + c) * ES + row] = v[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (16 * j + c < a.M) dst[static_cast<size_t>(16 * j + c) * kTileN] = v[c];
+        }
+      }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&acc_empty[b]);  // the MMA warp may reuse this accumulator
-      if (u.nseg == 1) {
-        // token-major staging: a warp's 32 rows of one token are 128 contiguous bytes
-#pragma unroll
-        for (int c = 0; c < NT * 16; ++c) E[c * ES + row] = v[c];
-      } else {
-        // this split's fp32 partial tile, token-major [t][row]: coalesced
-        float* dst = a.partials + (static_cast<size_t>(tile) * a.seg_max + u.seg) * Mp * kTileN + row;
-#pragma unroll
-        for (int c = 0; c < NT * 16; ++c)
-          if (c < a.M) dst[static_cast<size_t>(c) * kTileN] = v[c];
+      if (u.nseg != 1) {
         epi_bar();  // all partial stores of the CTA precede the releasing atomic
         if (et == 0) {
           int old;
@@ -232,27 +236,62 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         // 16-token tile at a time, its 16 loads per split in flight together.
         const float* src = a.partials + static_cast<size_t>(tile) * a.seg_max * Mp * kTileN + row;
         const size_t sstride = static_cast<size_t>(Mp) * kTileN;
-#pragma unroll 1
-        for (int j = 0; j < NT; ++j) {
-          if (16 * j >= a.M) break;
-          float acc[16];
+        if (a.M <= 4) {
+          // short windows: up to 8 splits' (<= 4) values in flight at once,
+          // then summed in split order -- the same additions as below, one
+          // L2 round trip instead of one per split (the tail of the GEMM)
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int sg0 = 0; sg0 < u.nseg; sg0 += 8) {
+            float p[8][4];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) acc[c] = 0.f;
-          for (int sg = 0; sg < u.nseg; ++sg) {
-            float p[16];
+            for (int q = 0; q < 8; ++q)
 #pragma unroll
-            for (int c = 0; c < 16; ++c)
-              p[c] = (16 * j + c < a.M) ? __ldcg(src + sg * sstride + static_cast<size_t>(16 * j + c) * kTileN) : 0.f;
+              for (int c = 0; c < 4; ++c)
+                p[q][c] = (sg0 + q < u.nseg && c < a.M)
+                              ? __ldcg(src + (sg0 + q) * sstride + static_cast<size_t>(c) * kTileN) : 0.f;
 #pragma unroll
-            for (int c = 0; c < 16; ++c) acc[c] += p[c];
+            for (int q = 0; q < 8; ++q)
+              if (sg0 + q < u.nseg)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[c] += p[q][c];
           }
 #pragma unroll
-          for (int c = 0; c < 16; ++c) E[(16 * j + c) * ES + row] = acc[c];
+          for (int c = 0; c < 4; ++c) E[c * ES + row] = acc[c];
+        } else {
+#pragma unroll 1
+          for (int j = 0; j < NT; ++j) {
+            if (16 * j >= a.M) break;
+            float acc[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[c] = 0.f;
+            // SGB splits' 16 values in flight per round, summed in split order
+            constexpr int SGB = NT == 1 ? 4 : 2;
+            for (int sg = 0; sg < u.nseg; sg += SGB) {
+              float p[SGB][16];
+#pragma unroll
+              for (int q = 0; q < SGB; ++q)
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                  p[q][c] = (sg + q < u.nseg && 16 * j + c < a.M)
+                                ? __ldcg(src + (sg + q) * sstride + static_cast<size_t>(16 * j + c) * kTileN) : 0.f;
+#pragma unroll
+              for (int q = 0; q < SGB; ++q)
+                if (sg + q < u.nseg)
+#pragma unroll
+                  for (int c = 0; c < 16; ++c) acc[c] += p[q][c];
+            }
+#pragma unroll
+            for (int c = 0; c < 16; ++c) E[(16 * j + c) * ES + row] = acc[c];
+          }
         }
         if (et == 0) a.flags[tile] = 0;
       }
       epi_bar();
-      epilogue_tile<NT * 4, true>(a.e, tile, E, ES, a.M, a.N, et, rsp);
+      if (NT <= 4) {
+        epilogue_tile<NT * 4, true>(a.e, tile, E, ES, a.M, a.N, et, rsp);
+      } else {  // 64-token slices: 16 items per thread at a time
+        for (int t0 = 0; t0 < a.M; t0 += 64) epilogue_tile<16, true>(a.e, tile, E, ES, a.M, a.N, et, rsp, t0);
+      }
       epi_bar();
     }
   }

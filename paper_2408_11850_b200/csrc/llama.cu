@@ -540,13 +540,8 @@ __device__ __forceinline__ void attn_item_m1(const AttnArgs& a, int kvh, int CS,
     cta_fold<HD>(st_c, cs_c, wgt_c, R, threadIdx.x - c * kAttnThreads, kAttnThreads,
                  [c] { asm volatile("bar.sync %0, %1;" ::"r"(3 + c), "r"(kAttnThreads) : "memory"); });
   __syncthreads();
-  float* cw = sm + 4 * Smem<HD>::kCtaFloats;
   auto peer = [&](int x) -> const float* { return sm + x * Smem<HD>::kCtaFloats + kWarps * kAttnMaxRb * RS; };
-  cluster_weights<HD>(peer, CS, R, cw, threadIdx.x);
-  __syncthreads();
-  cluster_sums<HD>(peer, CS, R, cw, threadIdx.x);
-  __syncthreads();
-  for (int cr = 0; cr < CS; ++cr) cluster_out<HD>(a, peer, CS, cr, R, 0, g, kvh, cw, threadIdx.x, kDraftThreads);
+  for (int cr = 0; cr < CS; ++cr) cluster_fold_out<HD>(a, peer, CS, cr, R, 0, g, kvh, threadIdx.x, kDraftThreads);
   __syncthreads();
 }
 

@@ -412,7 +412,7 @@ class LlamaModel(SequenceModel):
 
     def close(self) -> None:
         if getattr(self, "handle", None):
-            _lib.load().pearl_llama_destroy(self.handle)
+            _destroy_handle(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -420,6 +420,29 @@ class LlamaModel(SequenceModel):
             self.close()
         except Exception:
             pass
+
+
+# Handles whose release fell inside a CUDA graph capture (a garbage-collected
+# model while another model's step graph is being captured): cudaFree is not
+# capturable, so they are destroyed at the next release outside a capture.
+_PENDING_DESTROY: List[int] = []
+
+
+def _capturing() -> bool:
+    try:
+        return torch.cuda.is_available() and torch.cuda.is_current_stream_capturing()
+    except Exception:
+        return False
+
+
+def _destroy_handle(handle) -> None:
+    if _capturing():
+        _PENDING_DESTROY.append(handle)
+        return
+    lib = _lib.load()
+    while _PENDING_DESTROY:
+        lib.pearl_llama_destroy(_PENDING_DESTROY.pop())
+    lib.pearl_llama_destroy(handle)
 
 
 _FWD_ADVANCE = 1
