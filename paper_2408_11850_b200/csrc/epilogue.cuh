@@ -164,18 +164,21 @@ __device__ __forceinline__ float4 scale4(float4 v, float r) {
 // rs: per-token norm scales in smem (nullptr: no folded norm).
 // t_base: this call covers tokens t_base .. min(M, t_base + MAXI * 4) - 1
 // (wide windows run it in 64-token slices, bounding the registers per thread).
-template <int MAXI, bool TR = false>
+// NTHR: the epilogue threads sharing the items (idx = et + NTHR i); a call
+// covers up to MAXI * NTHR / 32 tokens.
+template <int MAXI, bool TR = false, int NTHR = 128>
 __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const float* E, int ES, int M, int N,
                                               int et, const float* rs = nullptr, int t_base = 0) {
   constexpr int kGroups = 32;  // 128 rows / 4
+  constexpr int kTok = MAXI * NTHR / kGroups;
   E += static_cast<size_t>(t_base) * (TR ? ES : 1);
   if (rs) rs += t_base;
-  const int nitems = kGroups * (M - t_base < MAXI * 4 ? M - t_base : MAXI * 4);
+  const int nitems = kGroups * (M - t_base < kTok ? M - t_base : kTok);
   switch (e.kind) {
     case EPI_STORE_F32:
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
-        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        const int idx = et + NTHR * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
         float* o = e.out_f32 + static_cast<size_t>(t_base + t) * e.ld + n0;
         float4 v = epi_rows4<TR>(E, ES, g, t);
@@ -193,13 +196,13 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       float4 hv[MAXI];
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
-        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        const int idx = et + NTHR * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx < nitems && n0 + 3 < N)
           hv[i] = *reinterpret_cast<const float4*>(e.out_f32 + static_cast<size_t>(t_base + t) * e.ld + n0);
       }
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
-        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        const int idx = et + NTHR * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems) continue;  // uniform per warp: a warp's 32 lanes are one token's 32 groups
         float4 hn = make_float4(0.f, 0.f, 0.f, 0.f);
         if (n0 < N) {
@@ -231,7 +234,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
     case EPI_SWIGLU:
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
-        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        const int idx = et + NTHR * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
         float4 v = epi_rows4<TR>(E, ES, g, t);
         if (rs) v = scale4(v, rs[t]);
@@ -245,7 +248,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       float2 cs[MAXI], sn[MAXI];
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
-        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        const int idx = et + NTHR * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx < nitems && n0 < e.n_q + e.n_kv) {
           const size_t off = static_cast<size_t>(e.tok_pos ? e.tok_pos[t_base + t] : p0 + t_base + t) * half + ((n0 % e.hd) >> 1);
           cs[i] = *reinterpret_cast<const float2*>(e.cos_t + off);
@@ -254,7 +257,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       }
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
-        const int idx = et + 128 * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
+        const int idx = et + NTHR * i, g = idx % kGroups, t = idx / kGroups, n0 = tile * 128 + g * 4;
         if (idx >= nitems || n0 >= N) continue;
         const int p = e.tok_pos ? e.tok_pos[t_base + t] : p0 + t_base + t;
         const size_t so = epi_slot_off(e, t_base + t);

@@ -58,7 +58,7 @@ __device__ __forceinline__ void tma_load_w(void* dst, const CUtensorMap* map, ui
 
 // ---- kernel ------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
+__global__ void __launch_bounds__(TcCfg<NT>::kThreads, TcCfg<NT>::kMinBlocks)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcArgs a) {
   using C = TcCfg<NT>;
   constexpr int stage_bytes = C::kStageBytes;
@@ -68,12 +68,15 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
   __shared__ float s_rs[kMaxTokTiles * kTokTile];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  float* E = reinterpret_cast<float*>(smem + stages * stage_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes + C::kEBytes);
+  unsigned char* xring = smem + stages * stage_bytes;  // kSplitX: [kXStages][NT x 2 KB]
+  float* E = reinterpret_cast<float*>(xring + C::kXRingBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xring + C::kXRingBytes + C::kEBytes);
   uint64_t* empty = full + kMaxStages;
   uint64_t* acc_full = empty + kMaxStages;   // [kAccs]
   uint64_t* acc_empty = acc_full + kAccs;    // [kAccs]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kAccs);
+  uint64_t* xfull = acc_empty + kAccs;       // [kXStages] (kSplitX)
+  uint64_t* xempty = xfull + C::kXStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + C::kXStages);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -89,7 +92,11 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
     }
     for (int b = 0; b < kAccs; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], kEpiThreads);
+      mbar_init(&acc_empty[b], C::kEpi);
+    }
+    for (int b = 0; b < C::kXStages; ++b) {
+      mbar_init(&xfull[b], 1);
+      mbar_init(&xempty[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
@@ -118,6 +125,42 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
       const int npre = min(stages, total);
       const int kb_start = static_cast<int>(r0 % a.KB), tile_start = static_cast<int>(r0 / a.KB);
       int kb = kb_start, tile = tile_start;
+      if constexpr (C::kSplitX) {
+        // W ring `stages` deep, X ring kXStages deep: X of iteration c is issued
+        // together with W of iteration c + D (D = stages - kXStages), both
+        // waiting on MMA(c + D - stages), so neither ring can wait on the other
+        constexpr int XS = C::kXStages;
+        constexpr int D = stages - XS;
+        static_assert(D >= 0, "W ring shallower than the X ring");
+        int xi = 0, kx = kb_start;
+        auto issue_x = [&]() {
+          const int sx = xi % XS;
+          if (xi >= XS) mbar_wait(&xempty[sx], ((xi / XS) - 1) & 1);
+          unsigned char* xs = xring + sx * C::kXStageBytes;
+          mbar_expect_tx(&xfull[sx], C::kXStageBytes);
+          tma_load_2d(xs, &tmX, &xfull[sx], kx * kTileK, 0);  // one box of 16 NT token rows
+          if (++kx == a.KB) kx = 0;
+          ++xi;
+        };
+        for (int it = 0; it < npre; ++it) {
+          mbar_expect_tx(&full[it], kWBytes);
+          tma_load_w(smem + it * stage_bytes, &tmW, &full[it], a, tile, kb);
+          if (++kb == a.KB) { kb = 0; ++tile; }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        PEARL_TL(a.tl, 1);
+        if (blockIdx.x == 0 && a.e.adv_pos != nullptr) *a.e.adv_pos += a.e.adv_n;
+        while (xi < total && xi < XS) issue_x();
+        for (int it = npre; it < total; ++it) {
+          const int s = it % stages;
+          mbar_wait(&empty[s], ((it / stages) - 1) & 1);
+          mbar_expect_tx(&full[s], kWBytes);
+          tma_load_w(smem + s * stage_bytes, &tmW, &full[s], a, tile, kb);
+          if (++kb == a.KB) { kb = 0; ++tile; }
+          if (xi < total && xi <= it - D) issue_x();
+        }
+        while (xi < total) issue_x();
+      } else {
       // W does not depend on the previous kernel: request it before the PDL wait
       for (int it = 0; it < npre; ++it) {
         unsigned char* st = smem + it * stage_bytes;
@@ -131,7 +174,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
       int kx = kb_start;
       for (int it = 0; it < npre; ++it) {
         unsigned char* st = smem + it * stage_bytes;
-        for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[it], kx * kTileK, j * kTokTile);
+        tma_load_2d(st + kWBytes, &tmX, &full[it], kx * kTileK, 0);  // one box of 16 NT token rows
         if (++kx == a.KB) kx = 0;
       }
       for (int it = npre; it < total; ++it) {
@@ -141,8 +184,9 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         const int kc = kb * kTileK;
         mbar_expect_tx(&full[s], bytes);
         tma_load_w(st, &tmW, &full[s], a, tile, kb);
-        for (int j = 0; j < NT; ++j) tma_load_2d(st + kWBytes + j * kXBytes, &tmX, &full[s], kc, j * kTokTile);
+        tma_load_2d(st + kWBytes, &tmX, &full[s], kc, 0);
         if (++kb == a.KB) { kb = 0; ++tile; }
+      }
       }
     }
   } else if (warp == 1) {
@@ -159,6 +203,8 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         for (int kb = u.kb0; kb < u.kb1; ++kb, ++it) {
           const int s = it % stages;
           mbar_wait(&full[s], (it / stages) & 1);
+          const int sx = it % C::kXStages;
+          if constexpr (C::kSplitX) mbar_wait(&xfull[sx], (it / C::kXStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           unsigned char* st = smem + s * stage_bytes;
 #ifdef PEARL_TIMELINE
@@ -168,30 +214,36 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
           // all NT token tiles in ONE MMA of N = 16 NT columns (the tiles are
           // contiguous rows of one SW128 operand); per-column arithmetic is the
           // same for any N (tests/test_gemm_gpu.py::test_batch_invariance)
-          const uint64_t bdesc = umma_desc_sw128(st + kWBytes);
+          const uint64_t bdesc =
+              umma_desc_sw128(C::kSplitX ? xring + sx * C::kXStageBytes : st + kWBytes);
 #pragma unroll
           for (int kk = 0; kk < kTileK / 16; ++kk)
             umma_bf16_n(acc, adesc + 2 * kk, bdesc + 2 * kk, (kb > u.kb0 || kk > 0) ? 1u : 0u,
                         umma_idesc(NT * kTokTile));
           umma_commit(&empty[s]);
+          if constexpr (C::kSplitX) umma_commit(&xempty[sx]);
         }
         umma_commit(&acc_full[b]);
       }
       PEARL_TL(a.tl, 3);
     }
   } else {
-    // ---- epilogue warps 2..5
+    // ---- epilogue warps 2..(2 + kEpiWarps); with 8 of them, warps w and
+    // w + 4 read the same TMEM lane quarter and take alternate token chunks
+    constexpr int EPI = C::kEpi;
+    constexpr int HALVES = C::kEpiWarps / 4;
     const int lanegrp = warp & 3;  // TMEM lane quarter this warp may access
     const int row = lanegrp * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127
+    const int et = threadIdx.x - 64;  // 0..EPI-1
+    const int half = et / 128;
     const int Mp = (a.M + 3) & ~3;  // partial row stride (float4 aligned)
     // folded RMSNorm: the per-token scales, once per CTA, while the first
     // accumulator is still being filled
     const float* rsp = nullptr;
     if (a.e.ss_in != nullptr) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
-      for (int t = et; t < a.M; t += kEpiThreads) s_rs[t] = norm_rs(a.e, t);
-      epi_bar();
+      for (int t = et; t < a.M; t += EPI) s_rs[t] = norm_rs(a.e, t);
+      epi_bar_n<EPI>();
       rsp = s_rs;
     }
     int ui = 0;
@@ -207,7 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
       // 128 contiguous bytes) or this split's fp32 partial [t][row] (coalesced)
       float* dst = a.partials + (static_cast<size_t>(tile) * a.seg_max + u.seg) * Mp * kTileN + row;
 #pragma unroll 1
-      for (int j = 0; j < NT; ++j) {
+      for (int j = half; j < NT; j += HALVES) {
         float v[16];
         tmem_ld16(tmem + (static_cast<uint32_t>(lanegrp * 32) << 16) + b * NT * kTokTile + j * kTokTile, v);
         if (u.nseg == 1) {
@@ -222,13 +274,13 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&acc_empty[b]);  // the MMA warp may reuse this accumulator
       if (u.nseg != 1) {
-        epi_bar();  // all partial stores of the CTA precede the releasing atomic
+        epi_bar_n<EPI>();  // all partial stores of the CTA precede the releasing atomic
         if (et == 0) {
           int old;
           asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.flags + tile) : "memory");
           *s_last = (old == u.nseg - 1);
         }
-        epi_bar();
+        epi_bar_n<EPI>();
         if (!*s_last) continue;
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         // Fixed split order => independent of arrival order and of M: each
@@ -257,6 +309,39 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
           }
 #pragma unroll
           for (int c = 0; c < 4; ++c) E[c * ES + row] = acc[c];
+        } else if (a.M > 16) {
+          // wide windows / prefill: every (token, 4-row group) item of the
+          // tile as a float4 (item idx = et + 128 i: the epilogue's mapping),
+          // 8 items' loads in flight per round, splits added in order
+          const float* base = a.partials + static_cast<size_t>(tile) * a.seg_max * Mp * kTileN;
+          const int nit = (32 * a.M - et + EPI - 1) / EPI;
+          for (int i0 = 0; i0 < nit; i0 += 8) {
+            float4 acc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int sg = 0; sg < u.nseg; ++sg) {
+              float4 pv[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int idx = et + EPI * (i0 + q);
+                pv[q] = i0 + q < nit ? __ldcg(reinterpret_cast<const float4*>(
+                                           base + sg * sstride + static_cast<size_t>(idx / 32) * kTileN + 4 * (idx % 32)))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                acc[q].x += pv[q].x;
+                acc[q].y += pv[q].y;
+                acc[q].z += pv[q].z;
+                acc[q].w += pv[q].w;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int idx = et + EPI * (i0 + q);
+              if (i0 + q < nit) *reinterpret_cast<float4*>(E + (idx / 32) * ES + 4 * (idx % 32)) = acc[q];
+            }
+          }
         } else {
 #pragma unroll 1
           for (int j = 0; j < NT; ++j) {
@@ -286,13 +371,13 @@ __global__ void __launch_bounds__(kTcThreads, TcCfg<NT>::kMinBlocks)
         }
         if (et == 0) a.flags[tile] = 0;
       }
-      epi_bar();
-      if (NT <= 4) {
-        epilogue_tile<NT * 4, true>(a.e, tile, E, ES, a.M, a.N, et, rsp);
-      } else {  // 64-token slices: 16 items per thread at a time
-        for (int t0 = 0; t0 < a.M; t0 += 64) epilogue_tile<16, true>(a.e, tile, E, ES, a.M, a.N, et, rsp, t0);
+      epi_bar_n<EPI>();
+      if (NT <= 2) {
+        epilogue_tile<NT * 4, true, EPI>(a.e, tile, E, ES, a.M, a.N, et, rsp);
+      } else {  // 64-token slices: 8 items per thread at a time over the 8 warps
+        for (int t0 = 0; t0 < a.M; t0 += 64) epilogue_tile<8, true, EPI>(a.e, tile, E, ES, a.M, a.N, et, rsp, t0);
       }
-      epi_bar();
+      epi_bar_n<EPI>();
     }
   }
   __syncwarp();
@@ -468,8 +553,11 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
     if (rc) return rc;
     it = ctx.wmaps.emplace(key, wm).first;
   }
+  // the window's NT token tiles as ONE box (16 NT rows of 128 B; the SW128
+  // layout of stacked 16-row boxes and of one tall box is the same), so the
+  // producer issues one X copy per stage instead of NT
   alignas(64) CUtensorMap xmap;
-  int rc = encode_2d(&xmap, X, K, M, kTokTile);
+  int rc = encode_2d(&xmap, X, K, M, kTokTile * ((M + kTokTile - 1) / kTokTile));
   if (rc) return rc;
   TcArgs a;
   a.M = M;
@@ -507,34 +595,42 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   switch (NT) {
     case 1:
       cfg.dynamicSmemBytes = TcCfg<1>::kSmem;
+      cfg.blockDim = dim3(TcCfg<1>::kThreads);
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<1>, it->second.map, xmap, a));
       break;
     case 2:
       cfg.dynamicSmemBytes = TcCfg<2>::kSmem;
+      cfg.blockDim = dim3(TcCfg<2>::kThreads);
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, it->second.map, xmap, a));
       break;
     case 3:
       cfg.dynamicSmemBytes = TcCfg<3>::kSmem;
+      cfg.blockDim = dim3(TcCfg<3>::kThreads);
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<3>, it->second.map, xmap, a));
       break;
     case 4:
       cfg.dynamicSmemBytes = TcCfg<4>::kSmem;
+      cfg.blockDim = dim3(TcCfg<4>::kThreads);
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<4>, it->second.map, xmap, a));
       break;
     case 5:
       cfg.dynamicSmemBytes = TcCfg<5>::kSmem;
+      cfg.blockDim = dim3(TcCfg<5>::kThreads);
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<5>, it->second.map, xmap, a));
       break;
     case 6:
       cfg.dynamicSmemBytes = TcCfg<6>::kSmem;
+      cfg.blockDim = dim3(TcCfg<6>::kThreads);
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<6>, it->second.map, xmap, a));
       break;
     case 7:
       cfg.dynamicSmemBytes = TcCfg<7>::kSmem;
+      cfg.blockDim = dim3(TcCfg<7>::kThreads);
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<7>, it->second.map, xmap, a));
       break;
     default:
       cfg.dynamicSmemBytes = TcCfg<8>::kSmem;
+      cfg.blockDim = dim3(TcCfg<8>::kThreads);
       PEARL_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<8>, it->second.map, xmap, a));
       break;
   }

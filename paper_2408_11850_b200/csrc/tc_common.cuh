@@ -17,7 +17,10 @@ constexpr int kTokTile = 16;   // tokens per MMA (MMA-N)
 constexpr int kMaxTokTiles = 8;  // windows / batched passes up to 128 tokens
 constexpr int kWBytes = kTileN * kTileK * 2;   // 16 KB
 constexpr int kXBytes = kTokTile * kTileK * 2; // 2 KB per token tile
-constexpr int kMaxStages = 8;
+#ifndef PEARL_MAX_STAGES
+#define PEARL_MAX_STAGES 8
+#endif
+constexpr int kMaxStages = PEARL_MAX_STAGES;
 constexpr int kTcThreads = 192;
 constexpr int kEpiThreads = 128;
 constexpr int kAccs = 4;  // TMEM accumulators (x NT*16 fp32 columns) in flight
@@ -37,16 +40,33 @@ constexpr int kAccs = 4;  // TMEM accumulators (x NT*16 fp32 columns) in flight
 #endif
 template <int NT>
 struct TcCfg {
+  // NT <= 2 (decode windows): W and X of a k-block share one stage of a
+  // 144 KB ring.  NT >= 3 (wide windows, prefill): X tiles would take up to
+  // half of every stage, halving the weight bytes in flight (latency-bound
+  // streaming: 4 stages = 64 KB of W per SM at NT = 8), so X gets its own
+  // 3-stage ring (L2-resident activations need little lead) and W keeps
+  // up to 8 x 16 KB stages.
+  static constexpr bool kSplitX = NT >= 3;
+  static constexpr int kXStages = 3;
+  static constexpr int kXStageBytes = NT * kXBytes;
   static constexpr int kRing = PEARL_RING_KB * 1024;
-  static constexpr int kStageBytes = kWBytes + NT * kXBytes;
-  static constexpr int kStages = (kRing / kStageBytes) < kMaxStages ? (kRing / kStageBytes) : kMaxStages;
   // staged tile, token-major: E[t * kEStride + row] (+4 pad keeps rows 16-byte aligned)
   static constexpr int kEStride = kTileN + 4;
   static constexpr int kEBytes = NT * 16 * kEStride * 4;
+  static constexpr int kStageBytes = kSplitX ? kWBytes : kWBytes + NT * kXBytes;
+  static constexpr int kXRingBytes = kSplitX ? kXStages * kXStageBytes : 0;
+  static constexpr int kBudget = 227 * 1024 - 1024 - 512 - kEBytes - kXRingBytes;
+  static constexpr int kStagesFit = kSplitX ? kBudget / kStageBytes : kRing / kStageBytes;
+  static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
   static constexpr int kCols = kAccs * NT * 16;
   static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
-  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + kEBytes + 512;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + kXRingBytes + kEBytes + 512;
   static constexpr int kMinBlocks = PEARL_GEMM_MINB;
+  // wide windows: 8 epilogue warps (each TMEM lane quarter read by two warps,
+  // one per half of the token chunks) for the 128-token tiles' epilogues
+  static constexpr int kEpiWarps = NT >= 2 ? 8 : 4;
+  static constexpr int kEpi = 32 * kEpiWarps;
+  static constexpr int kThreads = 64 + kEpi;
 };
 
 
@@ -140,6 +160,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
+template <int N>
+__device__ __forceinline__ void epi_bar_n() { asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory"); }
 
 // Stream-K: CTA c owns iterations [c*T/G, (c+1)*T/G) of the flattened
 // (tile, k-block) space.  cta_of(x) is the CTA whose range contains x.
