@@ -464,6 +464,28 @@ int tc_splits(int N, int K, int num_sms) {
   return best;
 }
 
+// Stream-K grid of an (N, K) GEMM on num_sms SMs -- a function of the shape
+// only (batch invariance).  Narrow GEMMs (fewer tiles than SMs / 2) whose
+// k-blocks divide evenly get tiles x S CTAs, every tile cut into exactly S
+// equal splits and every CTA owning one unit: no CTA straddles two tiles, so
+// the split-K last arrivers start together and the tail is one reduction
+// (7B O / down: 32 tiles x 4 splits on 128 CTAs).  Otherwise all SMs.
+int tc_grid(int N, int K, int num_sms) {
+  const int tiles = (N + kTileN - 1) / kTileN;
+  const int KB = (K + kTileK - 1) / kTileK;
+  const long long T = static_cast<long long>(tiles) * KB;
+  static const bool even = [] {
+    const char* env = std::getenv("PEARL_EVEN_SPLITS");  // 0: plain stream-K (A/B)
+    return !(env && env[0] == '0');
+  }();
+  if (even) {
+    for (int S = num_sms / tiles; S >= 2; --S) {
+      if (KB % S == 0 && KB / S >= 4 && tiles * S * 5 >= num_sms * 4) return tiles * S;
+    }
+  }
+  return static_cast<int>(std::min<long long>(num_sms, T));
+}
+
 // Largest number of stream-K segments any tile is cut into.
 int tc_seg_max(int tiles, int KB, int G) {
   const long long T = static_cast<long long>(tiles) * KB;
@@ -509,7 +531,7 @@ int tc_init(TcGemmCtx& ctx, const pearl_llama_config& c) {
   for (auto& s : shapes) {
     const int tiles = (s[0] + kTileN - 1) / kTileN;
     const int KB = (s[1] + kTileK - 1) / kTileK;
-    int Sa = tc_seg_max(tiles, KB, std::min<long long>(ctx.num_sms, static_cast<long long>(tiles) * KB));
+    int Sa = tc_seg_max(tiles, KB, tc_grid(s[0], s[1], ctx.num_sms));
     Sa = std::max(Sa, ctx.min_plan_splits);
     pf = std::max(pf, static_cast<size_t>(tiles) * Sa * kTileN * kMaxTokTiles * kTokTile);
     flags = std::max(flags, tiles);
@@ -566,7 +588,7 @@ int tc_gemm(TcGemmCtx& ctx, const __nv_bfloat16* W, const __nv_bfloat16* X, int 
   a.KB = (K + kTileK - 1) / kTileK;
   const int tiles = (N + kTileN - 1) / kTileN;
   a.T = static_cast<long long>(tiles) * a.KB;
-  a.G = static_cast<int>(std::min<long long>(force_splits > 0 ? force_splits : ctx.num_sms, a.T));
+  a.G = force_splits > 0 ? static_cast<int>(std::min<long long>(force_splits, a.T)) : tc_grid(N, K, ctx.num_sms);
   a.seg_max = tc_seg_max(tiles, a.KB, a.G);
   a.w_tiled = w_tiled ? 1 : 0;
   a.e = e;
