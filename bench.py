@@ -788,17 +788,19 @@ def run_reference(args):
     del shared
     greedy = args.temperature <= 0
     temp = 1.0 if greedy else args.temperature
-    P = args.cpu_prompt
-    mt = OracleLlama(tc, tw, device="cpu", max_seq=P + args.cpu_new + 64, mm_dtype=torch.bfloat16, temperature=temp)
-    md = OracleLlama(dc, dw, device="cpu", max_seq=P + args.cpu_new + 64, mm_dtype=torch.bfloat16, temperature=temp)
+    # the GPU arm's workload (prompt, new tokens, pair, temperature), one
+    # decode per step; the reference engine drafts a fixed gamma (it has no
+    # planner): the GPU arm's best fixed gamma on this pair
+    P, N, g = args.prompt, args.new, args.ref_gamma
+    mt = OracleLlama(tc, tw, device="cpu", max_seq=P + N + 2 * g + 64, mm_dtype=torch.bfloat16, temperature=temp)
+    md = OracleLlama(dc, dw, device="cpu", max_seq=P + N + 2 * g + 64, mm_dtype=torch.bfloat16, temperature=temp)
     prompts = _prompts(args.warmup + args.steps, P, tc.vocab, seed=1000)
     for i in range(min(args.warmup, 1)):
-        oe.decode_pearl(md, mt, prompts[i], args.gamma, 2, seed=i, greedy=greedy)
+        oe.decode_pearl(md, mt, prompts[i], g, 2, seed=i, greedy=greedy)
     t0 = time.perf_counter()
     toks = 0
     for i in range(args.steps):
-        out, _ = oe.decode_pearl(md, mt, prompts[args.warmup + i], args.gamma, args.cpu_new, seed=17 + i,
-                                 greedy=greedy)
+        out, _ = oe.decode_pearl(md, mt, prompts[args.warmup + i], g, N, seed=17 + i, greedy=greedy)
         toks += len(out)
     dt = time.perf_counter() - t0
     v = toks / dt
@@ -806,10 +808,14 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic prompts, random-init weights",
-            "config": {"workload": f"{args.pair} PEARL on host CPU cores, bounded sample", "pair": args.pair,
-                       "prompt_len": P, "new_tokens": args.cpu_new, "gamma": args.gamma},
+            "config": {"workload": f"{args.pair} PEARL (reference engine restated, fixed gamma {g}) on host CPU "
+                                   f"cores, batch 1, prompt {P}, {N} new tokens, "
+                                   f"{'greedy T=0' if greedy else f'T={temp:g}'}",
+                       "pair": args.pair, "global_batch": 1, "prompt_len": P, "new_tokens": N, "gamma": g,
+                       "temperature": 0.0 if greedy else temp},
             "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} x decode_pearl of {args.cpu_new} tokens, prompt {P}"},
+                             "sample": f"{args.steps} x decode_pearl of {N} tokens, prompt {P}, gamma {g} "
+                                       f"(oracle/engine.py + PyTorch CPU bf16 Llama)"},
             "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return line
@@ -838,7 +844,9 @@ def main():
     ap.add_argument("--gemm-target", default="tcgen05")
     ap.add_argument("--draft-sms", type=int, default=None,
                     help="green-context SMs for PEARL's concurrent draft (default per pair, PAIR_DRAFT_SMS)")
-    ap.add_argument("--cpu-new", type=int, default=16)
+    ap.add_argument("--cpu-new", type=int, default=16, help="new tokens of the in-bench cpu_baseline sample")
+    ap.add_argument("--ref-gamma", type=int, default=16,
+                    help="--impl reference: the CPU reference engine's fixed draft length")
     ap.add_argument("--cpu-prompt", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",

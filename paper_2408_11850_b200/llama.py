@@ -107,13 +107,12 @@ PAIR_BRANCH_STD = {"llama2-7b/68m": 5e-4, "dsc-33b/1.3b": 1.7e-4, "llama3-70b/8b
 # SMs of the green-context partition PEARL's concurrent draft runs on (the
 # target keeps the rest; 0 = shared SMs; the driver rounds to 8-SM groups).  On
 # its own SMs the 68M draft stops competing with the target's GEMM CTAs for SM
-# slots, and enough of them let it keep up with long draft blocks
-# (tools/green_sweep.sh, current kernels, T=1: PEARL 1165 tok/s at 16-24 SMs,
-# 1285-1295 at 32, 1287-1365 at 40 with gamma 16-32, 1165-1288 at 48; the
-# target's stream-K grid shrinks with it -- AR 307 -> 298 tok/s at 40).
-# DSC-33B/1.3B (prompt 512): shared 130 tok/s, 48 SMs 163 (PEARL > SD on the same
-# model; AR 72.6 -> 66.3 on the 100-SM target).  Llama-3 (V = 128256) needs
-# 16-CTA clusters for its pick / verify, which a partition cannot host: shared SMs.
+# slots, and enough of them let it keep up with long draft blocks.  Round-2
+# sweep with the round-2 kernels (tools/gpu_draftsms.sh, T=1, live planner
+# calibration): PEARL 1158 / 1372 / 1378 / 1451 / 1341 tok/s at 16 / 24 / 32 /
+# 40 / 48 SMs.  DSC-33B/1.3B (prompt 512): 48 SMs (round 1: shared 130 tok/s, 48
+# SMs 163).  Llama-3 (V = 128256) needs 16-CTA clusters for its pick / verify,
+# which a partition cannot host: shared SMs.
 PAIR_DRAFT_SMS = {"llama2-7b/68m": 40, "dsc-33b/1.3b": 48, "llama3-70b/8b": 0, "tiny": 0}
 
 

@@ -47,10 +47,12 @@ def test_bench_line_contract():
 
 
 def test_reference_arm_line():
-    d = _run("--impl", "reference", "--pair", "tiny", "--steps", "1", "--warmup", "1", "--cpu-new", "4",
-             "--cpu-prompt", "16")
+    d = _run("--impl", "reference", "--pair", "tiny", "--steps", "1", "--warmup", "1", "--new", "8",
+             "--prompt", "16", "--ref-gamma", "4")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] in ("port", "reference")
+    # the reference arm runs the GPU arm's workload: same pair, prompt and new tokens
+    assert (d["config"]["pair"], d["config"]["prompt_len"], d["config"]["new_tokens"]) == ("tiny", 16, 8)
 
 
 def test_bench_split_pairs_four_ranks_one_gpu():
