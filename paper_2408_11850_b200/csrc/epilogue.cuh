@@ -69,9 +69,19 @@ __device__ __forceinline__ float tile_sumsq(float4 h) {
 }
 
 // rs[t] of token t from the producer's per-tile partial sums (fixed order).
+// The tile sums are loaded 16 at a time (independent loads in flight, one L2
+// round trip per 16 tiles instead of one per tile) and added in tile order.
 __device__ __forceinline__ float norm_rs(const EpiArgs& e, int t) {
   float tot = 0.f;
-  for (int k = 0; k < e.ss_tiles; ++k) tot += __ldcg(e.ss_in + static_cast<size_t>(k) * e.ss_ld + t);
+  for (int k0 = 0; k0 < e.ss_tiles; k0 += 16) {
+    float v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      v[q] = k0 + q < e.ss_tiles ? __ldcg(e.ss_in + static_cast<size_t>(k0 + q) * e.ss_ld + t) : 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (k0 + q < e.ss_tiles) tot += v[q];
+  }
   return 1.0f / sqrtf(tot / static_cast<float>(e.norm_d) + e.norm_eps);
 }
 

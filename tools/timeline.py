@@ -66,6 +66,11 @@ for i in range(n):
     rel = lambda x: (x - t0) / 1e3  # noqa: E731
     r = {"i": i, "kind": kinds[i], "ctas": int(live.sum()), "start_us": round(rel(start), 2), "end_us": round(rel(end), 2),
          "dur_us": round((end - start) / 1e3, 2)}
+    if kinds[i] == "attn":
+        w1 = st[:, 1][st[:, 1] > 0]
+        if len(w1):
+            r.update(wait_lo=round(rel(int(w1.min())), 2), wait_hi=round(rel(int(w1.max())), 2),
+                     exit_lo=round(rel(int(st[:, 4].min())), 2))
     if kinds[i] != "attn":
         w1 = st[:, 1][st[:, 1] > 0]
         m2, m3 = st[:, 2][st[:, 2] > 0], st[:, 3][st[:, 3] > 0]
