@@ -132,17 +132,21 @@ __global__ void __launch_bounds__(kAttnThreads, MINB) attn_kernel(AttnArgs a) {
     warp_pass<HD>(a, kc, vc, kvs, p0, r0, R, g, kvh, pmax, kAttnLCS, lc0 + l, warp, lane, a.spw,
                   l == 0 ? old_hi : -1, kb, vb, st + warp * kAttnMaxRb * RS);
     __syncthreads();
+    if (threadIdx.x == 0 && first && l == 0) PEARL_TL(a.tl, 2);
     cta_fold<HD>(st, cs + l * kAttnMaxRb * RS, wgt, R, threadIdx.x, kAttnThreads, [] { __syncthreads(); });
     __syncthreads();
   }
+  if (threadIdx.x == 0 && first) PEARL_TL(a.tl, 3);
   // fold of the kAttnLCS logical states in order (DSMEM across the cluster);
   // logical CTA lc produces head dims [lc HD / kAttnLCS, (lc + 1) HD / kAttnLCS)
   if (CS > 1) cluster.sync();
+  if (threadIdx.x == 0 && first) PEARL_TL(a.tl, 5);
   auto peer = [&](int c) -> const float* {
     return cluster.map_shared_rank(cs + (c % per) * kAttnMaxRb * RS, c / per);
   };
   for (int l = 0; l < per; ++l)
     cluster_fold_out<HD>(a, peer, kAttnLCS, lc0 + l, R, r0, g, kvh, threadIdx.x, kAttnThreads);
+  if (threadIdx.x == 0 && first) PEARL_TL(a.tl, 6);
   if (CS > 1) cluster.sync();  // the peers' states stay alive until every CTA has read them
   else __syncthreads();         // smem reuse by the next item
   first = false;

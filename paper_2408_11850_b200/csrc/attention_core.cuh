@@ -228,17 +228,35 @@ __device__ __forceinline__ void cta_fold(const float* st, float* cs, float* wgt,
     if (w == 0) cs[rr * RS + HD] = mx;
   }
   sync();
-#pragma unroll 4
-  for (int i = tid; i < R * (HD + 1); i += nthr) {
-    const int rr = i / (HD + 1), d = i % (HD + 1);  // d == HD: the row's l
-    const int col = d < HD ? d : HD + 1;
-    float acc = 0.f;
+  // items in groups of 2: every load of the group before any store (the
+  // compiler cannot move a load above a store to the same shared array)
+  constexpr int G = 2;
+  const int n = R * (HD + 1);  // d == HD: the row's l
+  for (int i0 = tid; i0 < n; i0 += G * nthr) {
+    float wt[G][kWarps], sv[G][kWarps];
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const float wt = wgt[rr * kWarps + w];
-      if (wt != 0.f) acc = fmaf(wt, st[(w * kAttnMaxRb + rr) * RS + col], acc);
+    for (int q = 0; q < G; ++q) {
+      const int i = i0 + q * nthr;
+      const int rr = (i < n ? i : 0) / (HD + 1), d = (i < n ? i : 0) % (HD + 1);
+      const int col = d < HD ? d : HD + 1;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        wt[q][w] = wgt[rr * kWarps + w];
+        sv[q][w] = st[(w * kAttnMaxRb + rr) * RS + col];
+      }
     }
-    cs[rr * RS + col] = acc;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int i = i0 + q * nthr;
+      if (i >= n) break;
+      const int rr = i / (HD + 1), d = i % (HD + 1);
+      const int col = d < HD ? d : HD + 1;
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w)
+        if (wt[q][w] != 0.f) acc = fmaf(wt[q][w], sv[q][w], acc);
+      cs[rr * RS + col] = acc;
+    }
   }
 }
 
@@ -299,36 +317,52 @@ __device__ __forceinline__ void cluster_fold_out(const AttnArgs& a, Peer peer, i
                                                  int kvh, int tid, int nthr) {
   constexpr int RS = HD + 2;
   const int DC = HD / CS;
-#pragma unroll 4
-  for (int i = tid; i < R * DC; i += nthr) {
-    const int rr = i / DC, d = crank * DC + i % DC;
-    float m[kAttnCluster], l[kAttnCluster], o[kAttnCluster];
+  // items in groups of 4: all peers' (m, l, o) of the group loaded before any
+  // global store (a store through a generic pointer pins the loads after it)
+  constexpr int G = 4;
+  const int n = R * DC;
+  for (int i0 = tid; i0 < n; i0 += G * nthr) {
+    float m4[G][kAttnCluster], l4[G][kAttnCluster], o4[G][kAttnCluster];
 #pragma unroll
-    for (int c = 0; c < kAttnCluster; ++c) {
-      if (c < CS) {
-        const float* st = peer(c) + rr * RS;
-        m[c] = st[HD];
-        l[c] = st[HD + 1];
-        o[c] = st[d];
-      }
-    }
-    float mx = -INFINITY;
+    for (int q = 0; q < G; ++q) {
+      const int i = i0 + q * nthr < n ? i0 + q * nthr : i0;
+      const int rr = i / DC, d = crank * DC + i % DC;
 #pragma unroll
-    for (int c = 0; c < kAttnCluster; ++c)
-      if (c < CS) mx = fmaxf(mx, m[c]);
-    float L = 0.f, O = 0.f;
-#pragma unroll
-    for (int c = 0; c < kAttnCluster; ++c) {
-      if (c < CS) {
-        const float wt = m[c] == -INFINITY ? 0.f : expf(m[c] - mx);
-        if (wt != 0.f) {
-          L = fmaf(wt, l[c], L);
-          O = fmaf(wt, o[c], O);
+      for (int c = 0; c < kAttnCluster; ++c) {
+        if (c < CS) {
+          const float* st = peer(c) + rr * RS;
+          m4[q][c] = st[HD];
+          l4[q][c] = st[HD + 1];
+          o4[q][c] = st[d];
         }
       }
     }
-    const int r = r0 + rr, t = r / g, h = kvh * g + r % g;
-    a.o[(static_cast<size_t>(t) * a.H + h) * HD + d] = __float2bfloat16(O / L);
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int i = i0 + q * nthr;
+      if (i >= n) break;
+      const int rr = i / DC, d = crank * DC + i % DC;
+      const float* m = m4[q];
+      const float* l = l4[q];
+      const float* o = o4[q];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kAttnCluster; ++c)
+        if (c < CS) mx = fmaxf(mx, m[c]);
+      float L = 0.f, O = 0.f;
+#pragma unroll
+      for (int c = 0; c < kAttnCluster; ++c) {
+        if (c < CS) {
+          const float wt = m[c] == -INFINITY ? 0.f : expf(m[c] - mx);
+          if (wt != 0.f) {
+            L = fmaf(wt, l[c], L);
+            O = fmaf(wt, o[c], O);
+          }
+        }
+      }
+      const int r = r0 + rr, t = r / g, h = kvh * g + r % g;
+      a.o[(static_cast<size_t>(t) * a.H + h) * HD + d] = __float2bfloat16(O / L);
+    }
   }
 }
 

@@ -61,7 +61,9 @@ struct TcCfg {
   static constexpr int kCols = kAccs * NT * 16;
   static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes + kXRingBytes + kEBytes + 512;
-  static constexpr int kMinBlocks = PEARL_GEMM_MINB;
+  // NT = 1: registers capped for two CTAs per SM (<= 170), so the attention
+  // kernel (or the next GEMM after it) can be resident beside a GEMM CTA
+  static constexpr int kMinBlocks = NT == 1 ? 2 : PEARL_GEMM_MINB;
   // wide windows: 8 epilogue warps (each TMEM lane quarter read by two warps,
   // one per half of the token chunks) for the 128-token tiles' epilogues
   static constexpr int kEpiWarps = NT >= 2 ? 8 : 4;

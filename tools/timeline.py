@@ -71,6 +71,13 @@ for i in range(n):
         if len(w1):
             r.update(wait_lo=round(rel(int(w1.min())), 2), wait_hi=round(rel(int(w1.max())), 2),
                      exit_lo=round(rel(int(st[:, 4].min())), 2))
+            # per-phase medians over CTAs: wait -> warp passes -> CTA fold -> cluster sync -> fold out -> exit
+            ok = (st[:, 1] > 0) & (st[:, 2] > 0) & (st[:, 3] > 0) & (st[:, 5] > 0) & (st[:, 6] > 0)
+            if ok.any():
+                q = st[ok]
+                med = lambda a, b: round(float(np.median(q[:, b] - q[:, a])) / 1e3, 2)  # noqa: E731
+                r.update(ph_pass=med(1, 2), ph_ctafold=med(2, 3), ph_csync=med(3, 5), ph_foldout=med(5, 6),
+                         ph_exit=med(6, 4))
     if kinds[i] != "attn":
         w1 = st[:, 1][st[:, 1] > 0]
         m2, m3 = st[:, 2][st[:, 2] > 0], st[:, 3][st[:, 3] > 0]
