@@ -182,9 +182,17 @@ int attn_init() {
 }
 
 int attn_cluster_size(bool slot_mode) {
-  // slot mode (batched sequences): many short token runs, one item each --
-  // single-CTA clusters keep every item's latency chain short
-  if (slot_mode) return 1;
+  // slot mode (batched sequences): many short token runs, one item each.
+  // The fold is the same for any physical cluster (kAttnLCS logical CTAs),
+  // so this is purely a speed choice (PEARL_ATTN_CLUSTER_SLOT: 1, 2, 4).
+  if (slot_mode) {
+    static const int css = [] {
+      const char* v = std::getenv("PEARL_ATTN_CLUSTER_SLOT");
+      const int x = v ? std::atoi(v) : 1;
+      return (x == 1 || x == 2 || x == 4) ? x : 1;
+    }();
+    return css;
+  }
   static const int cs = [] {
     const char* v = std::getenv("PEARL_ATTN_CLUSTER");
     const int x = v ? std::atoi(v) : kAttnClusterDefault;
