@@ -7,6 +7,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <climits>
+
 namespace pearl {
 
 using bf16 = __nv_bfloat16;
@@ -176,9 +178,12 @@ __device__ __forceinline__ float4 scale4(float4 v, float r) {
 // (wide windows run it in 64-token slices, bounding the registers per thread).
 // NTHR: the epilogue threads sharing the items (idx = et + NTHR i); a call
 // covers up to MAXI * NTHR / 32 tokens.
+// pos0: the window's first position when the caller already read it (QKV,
+// sequence mode; INT_MIN: read *e.pos here).
 template <int MAXI, bool TR = false, int NTHR = 128>
 __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const float* E, int ES, int M, int N,
-                                              int et, const float* rs = nullptr, int t_base = 0) {
+                                              int et, const float* rs = nullptr, int t_base = 0,
+                                              int pos0 = INT_MIN) {
   constexpr int kGroups = 32;  // 128 rows / 4
   constexpr int kTok = MAXI * NTHR / kGroups;
   E += static_cast<size_t>(t_base) * (TR ? ES : 1);
@@ -203,6 +208,13 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       }
       break;
     case EPI_RESID: {
+      // a thread's items share their 4-row group g (NTHR is a multiple of
+      // 32), so the gain slice is one load, issued with the residual loads
+      float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
+      {
+        const int n0 = tile * 128 + (et % kGroups) * 4;
+        if (e.x_out && n0 + 3 < N) gv = __ldg(reinterpret_cast<const float4*>(e.gain + n0));
+      }
       float4 hv[MAXI];
 #pragma unroll
       for (int i = 0; i < MAXI; ++i) {
@@ -229,7 +241,6 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
         }
         if (e.x_out) {
           if (n0 + 3 < N) {
-            const float4 gv = __ldg(reinterpret_cast<const float4*>(e.gain + n0));  // same for every token: cached
             const __nv_bfloat162 lo = __floats2bfloat162_rn(hn.x * gv.x, hn.y * gv.y);
             const __nv_bfloat162 hi = __floats2bfloat162_rn(hn.z * gv.z, hn.w * gv.w);
             *reinterpret_cast<uint2*>(e.x_out + static_cast<size_t>(t_base + t) * e.ld + n0) =
@@ -253,7 +264,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiArgs& e, int tile, const 
       }
       break;
     case EPI_QKV: {
-      const int p0 = e.tok_pos ? 0 : *e.pos + e.pos_add;  // slot mode: per-token positions
+      const int p0 = e.tok_pos ? 0 : (pos0 != INT_MIN ? pos0 : *e.pos + e.pos_add);  // slot mode: per-token positions
       const int half = e.hd >> 1;
       float2 cs[MAXI], sn[MAXI];
 #pragma unroll

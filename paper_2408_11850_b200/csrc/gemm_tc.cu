@@ -246,6 +246,13 @@ __global__ void __launch_bounds__(TcCfg<NT>::kThreads, TcCfg<NT>::kMinBlocks)
       epi_bar_n<EPI>();
       rsp = s_rs;
     }
+    // QKV (sequence mode): the window's first position, read once (the
+    // epilogue's RoPE-table loads then need no dependent position load)
+    int pos0 = INT_MIN;
+    if (a.e.kind == EPI_QKV && a.e.tok_pos == nullptr) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      pos0 = *a.e.pos + a.e.pos_add;
+    }
     int ui = 0;
     for (long long x = r0; x < r1; ++ui) {
       const Unit u = unit_at(a, x, r1);
@@ -253,6 +260,7 @@ __global__ void __launch_bounds__(TcCfg<NT>::kThreads, TcCfg<NT>::kMinBlocks)
       const int tile = u.tile;
       const int b = ui % kAccs;
       mbar_wait(&acc_full[b], (ui / kAccs) & 1);
+      if (et == 0) PEARL_TL(a.tl, 5);  // (timeline builds) the last unit's accumulator is ready
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // the accumulator in 16-column chunks (16 registers live, not 16 NT):
       // token-major staging of the tile (a warp's 32 rows of one token are
@@ -282,7 +290,9 @@ __global__ void __launch_bounds__(TcCfg<NT>::kThreads, TcCfg<NT>::kMinBlocks)
         }
         epi_bar_n<EPI>();
         if (!*s_last) continue;
+        if (et == 0) PEARL_TL(a.tl, 6);  // (timeline builds) last arriver starts the reduction
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (et == 0) PEARL_TL(a.tl, 9);  // (timeline builds) past the acquire fence
         // Fixed split order => independent of arrival order and of M: each
         // element is ((0 + p_0) + p_1) + ... over the splits in order.  One
         // 16-token tile at a time, its 16 loads per split in flight together.
@@ -309,7 +319,7 @@ __global__ void __launch_bounds__(TcCfg<NT>::kThreads, TcCfg<NT>::kMinBlocks)
           }
 #pragma unroll
           for (int c = 0; c < 4; ++c) E[c * ES + row] = acc[c];
-        } else if (a.M > 16) {
+        } else if (a.M > 32) {
           // wide windows / prefill: every (token, 4-row group) item of the
           // tile as a float4 (item idx = et + 128 i: the epilogue's mapping),
           // 8 items' loads in flight per round, splits added in order
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(TcCfg<NT>::kThreads, TcCfg<NT>::kMinBlocks)
           }
         } else {
 #pragma unroll 1
-          for (int j = 0; j < NT; ++j) {
+          for (int j = half; j < NT; j += HALVES) {  // 8 warps: the two warps of a row take alternate chunks
             if (16 * j >= a.M) break;
             float acc[16];
 #pragma unroll
@@ -372,12 +382,15 @@ __global__ void __launch_bounds__(TcCfg<NT>::kThreads, TcCfg<NT>::kMinBlocks)
         if (et == 0) a.flags[tile] = 0;
       }
       epi_bar_n<EPI>();
+      if (et == 0) PEARL_TL(a.tl, 7);  // (timeline builds) tile staged in E
       if (NT <= 2) {
-        epilogue_tile<NT * 4, true, EPI>(a.e, tile, E, ES, a.M, a.N, et, rsp);
+        // MAXI * EPI / 32 = 16 NT tokens: exactly the window's tiles
+        epilogue_tile<NT * 512 / EPI, true, EPI>(a.e, tile, E, ES, a.M, a.N, et, rsp, 0, pos0);
       } else {  // 64-token slices: 8 items per thread at a time over the 8 warps
-        for (int t0 = 0; t0 < a.M; t0 += 64) epilogue_tile<8, true, EPI>(a.e, tile, E, ES, a.M, a.N, et, rsp, t0);
+        for (int t0 = 0; t0 < a.M; t0 += 64) epilogue_tile<8, true, EPI>(a.e, tile, E, ES, a.M, a.N, et, rsp, t0, pos0);
       }
       epi_bar_n<EPI>();
+      if (et == 0) PEARL_TL(a.tl, 8);  // (timeline builds) epilogue done
     }
   }
   __syncwarp();

@@ -104,3 +104,17 @@ for r in rows[5:10] + rows[-2:]:
     print("  ", r)
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(rows, open(f"gpurun_out/timeline_{name}_M{M}.json", "w"), indent=1)
+
+# latest-finishing CTAs of layer 1's GEMMs: last MMA (3), last accumulator seen by the
+# epilogue (5), last reduction start (6), exit (4)
+for i in (5, 7, 8, 9):
+    b = buf[i]
+    live = b[:, 0] > 0
+    if not live.any() or kinds[i] == "attn":
+        continue
+    st_ = b[live]
+    idx = np.argsort(-st_[:, 4])[:4]
+    rel = lambda x: round((int(x) - t0) / 1e3, 2) if x > 0 else None  # noqa: E731
+    print(f"  {kinds[i]:8s} latest: " + "; ".join(
+        f"mma_end {rel(st_[j, 3])} acc {rel(st_[j, 5])} reduce {rel(st_[j, 6])} fence {rel(st_[j, 9])} "
+        f"staged {rel(st_[j, 7])} epi {rel(st_[j, 8])} exit {rel(st_[j, 4])}" for j in idx))
