@@ -285,14 +285,16 @@ __global__ void __launch_bounds__(TcCfg<NT>::kThreads, TcCfg<NT>::kMinBlocks)
         epi_bar_n<EPI>();  // all partial stores of the CTA precede the releasing atomic
         if (et == 0) {
           int old;
-          asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.flags + tile) : "memory");
+          // release this CTA's partial stores (ordered before by the barrier)
+          // and, on the last arrival, acquire everyone else's: the CTA barrier
+          // below then orders every thread's partial loads after it
+          asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.flags + tile) : "memory");
           *s_last = (old == u.nseg - 1);
         }
         epi_bar_n<EPI>();
         if (!*s_last) continue;
         if (et == 0) PEARL_TL(a.tl, 6);  // (timeline builds) last arriver starts the reduction
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        if (et == 0) PEARL_TL(a.tl, 9);  // (timeline builds) past the acquire fence
+        if (et == 0) PEARL_TL(a.tl, 9);
         // Fixed split order => independent of arrival order and of M: each
         // element is ((0 + p_0) + p_1) + ... over the splits in order.  One
         // 16-token tile at a time, its 16 loads per split in flight together.
