@@ -1,9 +1,9 @@
-// K4 device core shared by the clustered attention kernel (attention.cu) and
-// the draft's persistent token forward (llama.cu, draft_fwd_kernel): one
-// warp's pass over its 32-position segments, the fold of a CTA's 4 warp
-// states, and the fold of the kAttnLCS logical CTA states.  Both callers run
-// exactly these instructions, so the persistent forward's attention rows are
-// bitwise the clustered kernel's (see attention.cuh for the algorithm).
+// K4 device core of the clustered attention kernel (attention.cu): one warp's
+// pass over its 32-position segments, the fold of a (logical) CTA's 4 warp
+// states, and the fold of the kAttnLCS logical CTA states (see attention.cuh
+// for the algorithm).  Kept apart so that every execution shape of the fold
+// (4-CTA clusters, one CTA running the logical CTAs in turn) runs exactly the
+// same instructions.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -25,8 +25,6 @@ struct Smem {
   static constexpr int kWarpFloats = kWarps * kAttnMaxRb * RS + kAttnMaxRb * kWarps;
   // one logical CTA's folded state [kAttnMaxRb][RS]
   static constexpr int kStateFloats = kAttnMaxRb * RS;
-  // per virtual CTA of the persistent forward: warp states + folded state + warp weights
-  static constexpr int kCtaFloats = kWarpFloats + kStateFloats;
   // cluster fold weights [kAttnMaxRb][kAttnCluster] + row sums [kAttnMaxRb]
   static constexpr int kFoldFloats = kAttnMaxRb * kAttnCluster + kAttnMaxRb;
 };

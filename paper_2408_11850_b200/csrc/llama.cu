@@ -43,7 +43,6 @@
 #include <vector>
 
 #include "attention.cuh"
-#include "attention_core.cuh"
 #include "common.h"
 #include "epilogue.cuh"
 #include "gemm_tc.cuh"
@@ -87,11 +86,6 @@ struct Llama {
   float* ss = nullptr;    // [ceil(d / 128), T] per-tile sums of h^2 (folded RMSNorm)
   int num_sms = 148;
   TcGemmCtx tc;           // tcgen05 path state (split-K scratch, descriptors)
-  // persistent single-token forward (CUDA-core models, draft_fwd_kernel)
-  int persist_grid = 0;   // co-resident CTAs (0: disabled)
-  LayerW* d_layers = nullptr;
-  float* hpriv = nullptr; // [persist_grid][d]
-  unsigned* gbar = nullptr;
 };
 
 // Optional per-op timing of an eager forward (pearl_llama_profile): an event
@@ -245,18 +239,17 @@ constexpr int kGemvMaxNormTok = 64;
 // full; the 4 rows an epilogue needs (SwiGLU / RoPE pairs) are then gathered
 // from 4 warps through shared memory.  Per-row arithmetic (chunk order, FMA
 // order, xor tree) is identical for every TOK and RPW (batch invariance).
-// The block-level body: block `bid` of a GEMV grid (also run by the draft's
-// persistent forward, draft_fwd_kernel, one virtual block at a time -- same
-// arithmetic, same bits).  Needs 8 warps; s_rs / s_out are the block's smem.
+// The block-level body: block `bid` of a GEMV grid.  Needs 8 warps; s_rs /
+// s_out are the block's smem.
 // Barrier of a GEMV block's 256 threads: the whole CTA (bar = 0) or named
-// barrier `bar` of one 256-thread group of a larger CTA (draft_fwd_kernel).
+// barrier `bar` of one 256-thread group of a larger CTA.
 __device__ __forceinline__ void grp_sync(int bar) {
   if (bar == 0) __syncthreads();
   else asm volatile("bar.sync %0, 256;" ::"r"(bar) : "memory");
 }
 
-// 16-byte load through L2 (no non-coherent path): X written earlier in the
-// same kernel (the persistent forward) must not be read with ld.global.nc.
+// 16-byte load through L2 (no non-coherent path), for an X written earlier
+// in the same kernel (COH = true), which must not be read with ld.global.nc.
 __device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
@@ -387,278 +380,6 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
   pdl_trigger();
   if (e.adv_pos != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *e.adv_pos += e.adv_n;
   gemv_block<TOK, RPW>(W, X, M, N, K, e, nrm, blockIdx.x, s_rs, s_out);
-}
-
-// ---------------------------------------------------------------------------
-// Persistent single-token forward of a CUDA-core (draft) model.
-//
-// The draft's _draft_block (engines.py:277-282) runs gamma one-token forwards
-// back to back; as separate launches (embed, 5 per layer, lm_head) each is a
-// few microseconds of weights behind a launch and a dependency drain.  Here
-// ONE launch runs the whole forward: a grid of co-resident 512-thread CTAs
-// (two 256-thread "virtual GEMV blocks" each) walks the phases
-//     [QKV, attention, O, gate/up, down] x L, lm_head
-// separated by grid barriers.  Every phase executes exactly the per-block
-// code of the multi-launch forward -- gemv_block for the contractions (same
-// virtual block -> row mapping, same FMA chains and xor trees, same fused
-// norm and epilogues), attn_core for attention with the CS CTAs of a cluster
-// emulated by CS 4-warp groups of one CTA and their DSMEM fold done in shared
-// memory -- so its logits are bitwise those of the multi-launch forward
-// (tests/test_llama_gpu.py::test_draft_persistent_forward_bitwise).  Weights
-// of the next phase are prefetched into L2 (cp.async.bulk.prefetch) before
-// the barrier that guards their activations.
-// ---------------------------------------------------------------------------
-constexpr int kDraftThreads = 512;
-constexpr int kDraftGroups = kDraftThreads / (kGemvWarps * 32);
-
-struct DraftFwdArgs {
-  const bf16* embed;
-  const float* final_norm;
-  const bf16* lm_head;
-  const float* cos_t;
-  const float* sin_t;
-  bf16* kcache;
-  bf16* vcache;
-  const LayerW* layers;  // device copy of the per-layer pointers
-  int L, d, H, KV, hd, ffn, V;
-  size_t layer_kv;       // elements per layer cache
-  float eps;
-  const int32_t* token;
-  int32_t* pos;
-  int adv;               // advance *pos by 1 at the end
-  float* logits;         // [V] or nullptr
-  float* h;              // [d] residual stream
-  float* hpriv;          // [grid][d] per-CTA copy of the embedding row
-  bf16* q;
-  bf16* o;
-  bf16* act;
-  unsigned* gbar;        // [0] arrivals, [1] generation
-  int spw, CS;           // attention plan (sequence mode, M = 1)
-  unsigned long long* tl;  // PEARL_TIMELINE builds: per-CTA phase stamps
-};
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Grid barrier over co-resident CTAs: arrival counter + generation flag (the
-// generation persists across launches; the last arriver resets the counter
-// before releasing).  Writes before it are visible to every CTA after it.
-__device__ __forceinline__ void grid_barrier(unsigned* gbar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned g0, old;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gbar + 1) : "memory");
-    // release: this CTA's writes (ordered before by bar.sync) reach whoever acquires
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(gbar) : "memory");
-    if (old == gridDim.x - 1) {
-      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(gbar) : "memory");
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar + 1) : "memory");
-    } else {
-      // every CTA must be co-resident (grid sized to the model's SMs); a
-      // barrier that cannot complete traps after 10 s instead of hanging
-      const unsigned long long t0 = tl_now();
-      while (ld_acquire_u32(gbar + 1) == g0) {
-        if (tl_now() - t0 > 10000000000ull) __trap();
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// launch_gemv's row blocking: narrow layers one row per warp (8 rows per
-// block), wide ones four (32 rows per block)
-__host__ __device__ __forceinline__ bool gemv_narrow(int N) {
-  return (N + kGemvWarps * kGemvRows - 1) / (kGemvWarps * kGemvRows) < 296;
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// Prefetch the weight rows this group's virtual blocks of a GEMV phase read.
-__device__ __forceinline__ void gemv_prefetch(const bf16* W, int N, int K, int slot, int slots, int tid) {
-  const int rpb = gemv_narrow(N) ? kGemvWarps : kGemvWarps * kGemvRows;
-  const int nb = (N + rpb - 1) / rpb;
-  int i = 0;
-  for (int vb = slot; vb < nb; vb += slots, ++i) {
-    if (tid != (i & 31)) continue;
-    const int r0 = vb * rpb, r1 = min(N, r0 + rpb);
-    const size_t bytes = static_cast<size_t>(r1 - r0) * K * sizeof(bf16);
-    prefetch_l2(W + static_cast<size_t>(r0) * K, static_cast<uint32_t>(bytes & ~static_cast<size_t>(15)));
-  }
-}
-
-// One GEMV phase: this group's virtual blocks slot, slot + slots, ...
-template <bool NARROW>
-__device__ __forceinline__ void gemv_phase_impl(const bf16* W, const bf16* X, int N, int K, const EpiArgs& e,
-                                                const GemvNorm& nrm, int slot, int slots, float* s_rs, float* s_out,
-                                                int tid, int bar) {
-  const int rpb = NARROW ? kGemvWarps : kGemvWarps * kGemvRows;
-  const int nb = (N + rpb - 1) / rpb;
-  for (int vb = slot; vb < nb; vb += slots)
-    gemv_block<1, NARROW ? 1 : 4, true>(W, X, 1, N, K, e, nrm, vb, s_rs, s_out, tid, bar);
-}
-
-__device__ __forceinline__ void gemv_phase(const bf16* W, const bf16* X, int N, int K, const EpiArgs& e,
-                                           const GemvNorm& nrm, int slot, int slots, float* s_rs, float* s_out,
-                                           int tid, int bar) {
-  if (gemv_narrow(N)) gemv_phase_impl<true>(W, X, N, K, e, nrm, slot, slots, s_rs, s_out, tid, bar);
-  else gemv_phase_impl<false>(W, X, N, K, e, nrm, slot, slots, s_rs, s_out, tid, bar);
-}
-
-// Attention of the single token for KV head kvh: the CS CTAs x 4 warps of the
-// clustered kernel's (row block 0, kvh) item, as CS 4-warp groups of this CTA.
-template <int HD>
-__device__ __forceinline__ void attn_item_m1(const AttnArgs& a, int kvh, int CS, float* sm) {
-  using namespace attn_core;
-  constexpr int J = HD / 32;
-  constexpr int RS = HD + 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = warp / kWarps, w = warp % kWarps;
-  const int g = a.H / a.KV;
-  const int R = g;  // one token: rows (0, j), j < g
-  const int p0 = *a.pos + a.pos_add;
-  const size_t kvs = static_cast<size_t>(a.KV) * HD;
-  const bf16* kc = a.kc + static_cast<size_t>(kvh) * HD;
-  const bf16* vc = a.vc + static_cast<size_t>(kvh) * HD;
-  float* st_c = sm + c * Smem<HD>::kCtaFloats;
-  float* cs_c = st_c + kWarps * kAttnMaxRb * RS;
-  float* wgt_c = cs_c + kAttnMaxRb * RS;
-  if (c < CS) {
-    uint4 kb[4][J], vb[4][J];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < J; ++j) kb[i][j] = vb[i][j] = make_uint4(0, 0, 0, 0);
-    warp_pass<HD>(a, kc, vc, kvs, p0, 0, R, g, kvh, p0, CS, c, w, lane, a.spw, -1, kb, vb, st_c + w * kAttnMaxRb * RS);
-  }
-  __syncthreads();
-  if (c < CS)
-    cta_fold<HD>(st_c, cs_c, wgt_c, R, threadIdx.x - c * kAttnThreads, kAttnThreads,
-                 [c] { asm volatile("bar.sync %0, %1;" ::"r"(3 + c), "r"(kAttnThreads) : "memory"); });
-  __syncthreads();
-  auto peer = [&](int x) -> const float* { return sm + x * Smem<HD>::kCtaFloats + kWarps * kAttnMaxRb * RS; };
-  for (int cr = 0; cr < CS; ++cr) cluster_fold_out<HD>(a, peer, CS, cr, R, 0, g, kvh, threadIdx.x, kDraftThreads);
-  __syncthreads();
-}
-
-template <int HD>
-__global__ void __launch_bounds__(kDraftThreads, 1) draft_fwd_kernel(DraftFwdArgs a) {
-  __shared__ float s_rs[kDraftGroups][kGemvMaxNormTok];
-  __shared__ float s_out[kDraftGroups][kGemvWarps];
-  extern __shared__ __align__(16) float attn_sm[];
-  const int grp = threadIdx.x / (kGemvWarps * 32), tid = threadIdx.x % (kGemvWarps * 32);
-  const int slots = gridDim.x * kDraftGroups, slot = blockIdx.x * kDraftGroups + grp;
-  const int bar = 1 + grp;
-  const int d = a.d, nq = a.H * a.hd, nkv = a.KV * a.hd;
-  int nb = 0;  // barriers passed (timeline stamps)
-  (void)nb;
-  if (threadIdx.x == 0) PEARL_TL(a.tl, 0);
-  // layer 0's QKV weights do not depend on the previous kernel
-  gemv_prefetch(a.layers[0].wqkv, nq + 2 * nkv, d, slot, slots, tid);
-  pdl_wait();
-  pdl_trigger();
-  if (threadIdx.x == 0) PEARL_TL(a.tl, 1);
-  // every CTA keeps its own copy of the embedding row for layer 0's fused
-  // norm (no barrier); CTA 0 also seeds the shared residual stream
-  {
-    int tok = *a.token;
-    tok = tok < 0 ? 0 : (tok >= a.V ? a.V - 1 : tok);
-    const bf16* row = a.embed + static_cast<size_t>(tok) * d;
-    float* hp = a.hpriv + static_cast<size_t>(blockIdx.x) * d;
-    for (int i = threadIdx.x; i < d; i += kDraftThreads) {
-      const float v = __bfloat162float(row[i]);
-      hp[i] = v;
-      if (blockIdx.x == 0) a.h[i] = v;
-    }
-    __syncthreads();
-  }
-  AttnArgs aa{};
-  aa.q = a.q;
-  aa.o = a.o;
-  aa.pos = a.pos;
-  aa.M = 1;
-  aa.H = a.H;
-  aa.KV = a.KV;
-  aa.scale = 1.0f / sqrtf(static_cast<float>(a.hd));
-  aa.tpb = 1;
-  aa.spw = a.spw;
-  for (int l = 0; l < a.L; ++l) {
-    const LayerW Lw = a.layers[l];
-    // ---- QKV (+ fused attn norm, RoPE, K/V append)
-    gemv_prefetch(Lw.wo, d, nq, slot, slots, tid);
-    EpiArgs e{};
-    e.kind = EPI_QKV;
-    e.out_bf16 = a.q;
-    e.kc = a.kcache + l * a.layer_kv;
-    e.vc = a.vcache + l * a.layer_kv;
-    e.cos_t = a.cos_t;
-    e.sin_t = a.sin_t;
-    e.pos = a.pos;
-    e.n_q = nq;
-    e.n_kv = nkv;
-    e.hd = a.hd;
-    gemv_phase(Lw.wqkv, nullptr, nq + 2 * nkv, d, e,
-               GemvNorm{l == 0 ? a.hpriv + static_cast<size_t>(blockIdx.x) * d : a.h, Lw.attn_norm, a.eps}, slot,
-               slots, s_rs[grp], s_out[grp], tid, bar);
-    grid_barrier(a.gbar);
-    if (threadIdx.x == 0 && nb < 12) PEARL_TL(a.tl, 2 + nb);
-    ++nb;
-    // ---- attention (one CTA per KV head)
-    gemv_prefetch(Lw.wgu, 2 * a.ffn, d, slot, slots, tid);
-    aa.kc = e.kc;
-    aa.vc = e.vc;
-    for (int item = blockIdx.x; item < a.KV; item += gridDim.x) attn_item_m1<HD>(aa, item, a.CS, attn_sm);
-    grid_barrier(a.gbar);
-    if (threadIdx.x == 0 && nb < 12) PEARL_TL(a.tl, 2 + nb);
-    ++nb;
-    // ---- O (+ residual)
-    gemv_prefetch(Lw.wdown, d, a.ffn, slot, slots, tid);
-    EpiArgs r{};
-    r.kind = EPI_RESID;
-    r.out_f32 = a.h;
-    r.ld = d;
-    gemv_phase(Lw.wo, a.o, d, nq, r, GemvNorm{nullptr, nullptr, 0.f}, slot, slots, s_rs[grp], s_out[grp], tid, bar);
-    grid_barrier(a.gbar);
-    if (threadIdx.x == 0 && nb < 12) PEARL_TL(a.tl, 2 + nb);
-    ++nb;
-    // ---- gate / up (+ fused mlp norm, SwiGLU)
-    if (l + 1 < a.L) gemv_prefetch(a.layers[l + 1].wqkv, nq + 2 * nkv, d, slot, slots, tid);
-    EpiArgs gu{};
-    gu.kind = EPI_SWIGLU;
-    gu.out_bf16 = a.act;
-    gu.ld = a.ffn;
-    gemv_phase(Lw.wgu, nullptr, 2 * a.ffn, d, gu, GemvNorm{a.h, Lw.mlp_norm, a.eps}, slot, slots, s_rs[grp],
-               s_out[grp], tid, bar);
-    grid_barrier(a.gbar);
-    if (threadIdx.x == 0 && nb < 12) PEARL_TL(a.tl, 2 + nb);
-    ++nb;
-    // ---- down (+ residual)
-    if (l + 1 == a.L && a.logits) gemv_prefetch(a.lm_head, a.V, d, slot, slots, tid);
-    EpiArgs dn{};
-    dn.kind = EPI_RESID;
-    dn.out_f32 = a.h;
-    dn.ld = d;
-    gemv_phase(Lw.wdown, a.act, d, a.ffn, dn, GemvNorm{nullptr, nullptr, 0.f}, slot, slots, s_rs[grp], s_out[grp],
-               tid, bar);
-    grid_barrier(a.gbar);
-    if (threadIdx.x == 0 && nb < 12) PEARL_TL(a.tl, 2 + nb);
-    ++nb;
-  }
-  // every reader of *pos (QKV epilogues, attention) is behind the last barrier
-  if (a.adv && blockIdx.x == 0 && threadIdx.x == 0) *a.pos += 1;
-  if (a.logits == nullptr) return;
-  EpiArgs s{};
-  s.kind = EPI_STORE_F32;
-  s.out_f32 = a.logits;
-  s.ld = a.V;
-  gemv_phase(a.lm_head, nullptr, a.V, d, s, GemvNorm{a.h, a.final_norm, a.eps}, slot, slots, s_rs[grp], s_out[grp],
-             tid, bar);
-  __syncthreads();
-  if (threadIdx.x == 0) PEARL_TL(a.tl, 15);
 }
 
 // ---------------------------------------------------------------------------
@@ -848,82 +569,6 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
   return rc;
 }
 
-template <int HD>
-size_t draft_fwd_smem() {
-  return static_cast<size_t>(4 * attn_core::Smem<HD>::kCtaFloats + attn_core::Smem<HD>::kFoldFloats) * sizeof(float);
-}
-
-// Set up the persistent single-token forward for a CUDA-core model
-// (opt-in: PEARL_DRAFT_PERSIST=1).  Needs every CTA co-resident: one
-// 512-thread CTA per SM of the model's partition.  Measured on B200 (68M,
-// tools/draft_timeline.py): 94-100 us per token against 72 us for the
-// multi-launch forward -- each of the 11 phases costs 5-10 us (a grid
-// barrier plus its virtual blocks' latency chains run one after another
-// on 2 x 256 threads per SM, where the separate launches run them all at
-// once at up to 2048 threads per SM), so it is not the default.
-int draft_persist_init(Llama& m) {
-  const auto& c = m.cfg;
-  const char* env = std::getenv("PEARL_DRAFT_PERSIST");
-  if (!(env && std::atoi(env) == 1)) return PEARL_OK;
-  if (c.gemm_kind != PEARL_GEMM_CUDACORE) return PEARL_OK;
-  void (*kern)(DraftFwdArgs) = c.head_dim == 128 ? draft_fwd_kernel<128> : draft_fwd_kernel<64>;
-  const size_t smem = c.head_dim == 128 ? draft_fwd_smem<128>() : draft_fwd_smem<64>();
-  PEARL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 0;
-  PEARL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDraftThreads, smem));
-  if (per_sm < 1) return PEARL_OK;
-  const int grid = m.num_sms;
-  std::vector<LayerW> lw(m.layers.begin(), m.layers.end());
-  PEARL_CUDA_TRY(cudaMalloc(&m.d_layers, lw.size() * sizeof(LayerW)));
-  PEARL_CUDA_TRY(cudaMemcpy(m.d_layers, lw.data(), lw.size() * sizeof(LayerW), cudaMemcpyHostToDevice));
-  PEARL_CUDA_TRY(cudaMalloc(&m.hpriv, static_cast<size_t>(grid) * c.d_model * sizeof(float)));
-  PEARL_CUDA_TRY(cudaMalloc(&m.gbar, 2 * sizeof(unsigned)));
-  PEARL_CUDA_TRY(cudaMemset(m.gbar, 0, 2 * sizeof(unsigned)));
-  m.persist_grid = grid;
-  return PEARL_OK;
-}
-
-int draft_forward_persistent(Llama& m, const int32_t* token, int32_t* pos, bool adv, float* logits, cudaStream_t st) {
-  const auto& c = m.cfg;
-  DraftFwdArgs a{};
-  a.embed = m.embed;
-  a.final_norm = m.final_norm;
-  a.lm_head = m.lm_head;
-  a.cos_t = m.rope_cos;
-  a.sin_t = m.rope_sin;
-  a.kcache = m.kcache;
-  a.vcache = m.vcache;
-  a.layers = m.d_layers;
-  a.L = c.n_layers;
-  a.d = c.d_model;
-  a.H = c.n_heads;
-  a.KV = c.n_kv_heads;
-  a.hd = c.head_dim;
-  a.ffn = c.ffn;
-  a.V = c.vocab;
-  a.layer_kv = static_cast<size_t>(std::max(1, c.n_slots)) * c.max_seq * c.n_kv_heads * c.head_dim;
-  a.eps = c.norm_eps;
-  a.token = token;
-  a.pos = pos;
-  a.adv = adv ? 1 : 0;
-  a.logits = logits;
-  a.h = m.h;
-  a.hpriv = m.hpriv;
-  a.q = m.q;
-  a.o = m.o;
-  a.act = m.act;
-  a.gbar = m.gbar;
-  int tpb = 1, agrid = 1;
-  attn_plan(AttnShape{1, c.n_heads, c.n_kv_heads, c.head_dim, c.max_seq, m.num_sms, false}, &tpb, &a.spw, &agrid);
-  a.CS = kAttnLCS;  // the fold's logical CTAs, whatever the physical cluster
-#ifdef PEARL_TIMELINE
-  a.tl = timeline_next(2);
-#endif
-  const bool h128 = c.head_dim == 128;
-  return launch_pdl(h128 ? draft_fwd_kernel<128> : draft_fwd_kernel<64>, dim3(m.persist_grid), dim3(kDraftThreads),
-                    h128 ? draft_fwd_smem<128>() : draft_fwd_smem<64>(), st, a);
-}
-
 }  // namespace
 }  // namespace pearl
 
@@ -995,12 +640,6 @@ extern "C" int pearl_llama_create(const pearl_llama_config* cfg, const void* con
       delete m;
       return rc;
     }
-  } else {
-    int rc = draft_persist_init(*m);
-    if (rc) {
-      delete m;
-      return rc;
-    }
   }
   *handle = m;
   return PEARL_OK;
@@ -1015,9 +654,6 @@ extern "C" int pearl_llama_destroy(void* handle) {
   cudaFree(m->o);
   cudaFree(m->act);
   cudaFree(m->ss);
-  if (m->d_layers) cudaFree(m->d_layers);
-  if (m->hpriv) cudaFree(m->hpriv);
-  if (m->gbar) cudaFree(m->gbar);
   tc_free(m->tc);
   delete m;
   return PEARL_OK;
@@ -1086,8 +722,6 @@ extern "C" int pearl_llama_forward(void* handle, const int32_t* tokens, int n_to
     explicit WindowScope(const L2Window& w) { g_l2win = w; }
     ~WindowScope() { g_l2win = L2Window{}; }
   } window_scope(m->l2win);
-  if (n_tokens == 1 && m->persist_grid > 0 && ablate_mask() == 0 && stop_after() < 0)
-    return draft_forward_persistent(*m, tokens, pos, (flags & PEARL_FWD_ADVANCE) != 0, logits, st);
   bool advanced = false;
   for (int c0 = 0; c0 < n_tokens; c0 += T) {
     const int mt = std::min(T, n_tokens - c0);

@@ -164,39 +164,3 @@ def test_adaptive_gamma_replays_exactly(pair):
     toks, steps = oe.decode_pearl(draft, target, prefix, 4, 64, 9, gamma_schedule=sched)
     assert list(res.tokens) == list(toks)
     assert _strip(res.steps) == steps
-
-
-@pytest.mark.parametrize("preset,max_seq", [("tiny-draft", 512), ("llama-68m", 700), ("llama-68m", 4096)])
-def test_draft_persistent_forward_bitwise(preset, max_seq):
-    """The persistent single-token forward of a CUDA-core model
-    (draft_fwd_kernel: one launch, grid barriers; PEARL_DRAFT_PERSIST=1)
-    gives bitwise the logits, K/V cache rows and position of the
-    multi-launch forward -- over a prompt, then 40 one-token steps whose
-    contexts cross several 128-position attention segments."""
-    import os
-    from paper_2408_11850_b200 import llama
-    cfg = llama.PRESETS[preset]
-    align = llama.AlignSpec(branch_std=0.02)
-    w = llama.init_weights(cfg, align, 5, "cuda", llama._shared_tables(cfg.vocab, align, "cuda"))
-    ref = llama.LlamaModel(cfg, w, gemm="cudacore", max_seq=max_seq, max_tokens=64)
-    os.environ["PEARL_DRAFT_PERSIST"] = "1"  # opt-in (not faster on B200: see llama.cu)
-    try:
-        fast = llama.LlamaModel(cfg, w, gemm="cudacore", max_seq=max_seq, max_tokens=64)
-    finally:
-        del os.environ["PEARL_DRAFT_PERSIST"]
-    rng = np.random.default_rng(3)
-    P = 200 if max_seq < 4096 else 3900
-    toks = torch.tensor([1] + rng.integers(2, cfg.vocab, P + 40).tolist(), dtype=torch.int32, device="cuda")
-    outs = []
-    for m in (fast, ref):
-        pos = torch.zeros(1, dtype=torch.int32, device="cuda")
-        m.forward(toks[:P], P, pos, 1, None)
-        lg = torch.empty(40, cfg.vocab, device="cuda")
-        for j in range(40):
-            m.forward(toks[P + j:P + j + 1], 1, pos, 1 | 2, lg[j:j + 1])
-        torch.cuda.synchronize()
-        outs.append((lg, int(pos.item()), m.k_cache.clone(), m.v_cache.clone()))
-    (a, pa, ka, va), (b, pb, kb, vb) = outs
-    assert pa == pb == P + 40
-    assert torch.equal(ka, kb) and torch.equal(va, vb)
-    assert torch.equal(a, b), float((a - b).abs().max())
