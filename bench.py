@@ -201,6 +201,11 @@ def run_gpu(args):
     # AR and SD never overlap two models: they run on the target over the
     # WHOLE GPU (its own stream-K grids), not on PEARL's partition
     target_full = target.clone(sm_count=0) if getattr(target, "green_partition", None) is not None else target
+    # likewise SD's draft: a tcgen05 draft built for PEARL's partition sizes its
+    # stream-K grids to it; SD runs it alone on the whole GPU (a CUDA-core draft's
+    # grids do not depend on the SM count)
+    draft_full = (draft.clone(sm_count=0)
+                  if getattr(target, "green_partition", None) is not None and draft.gemm == "tcgen05" else draft)
     V = target.cfg.vocab
     draft_sms_used = getattr(target, "green_partition", (None, None, 0, 0))[2]
     prompts = _prompts(args.warmup + args.steps, args.prompt, V, seed=1000 + rank)
@@ -220,7 +225,7 @@ def run_gpu(args):
         if kind.startswith("pearl"):
             return pk.decode_pearl(draft, target, prompts[i], cfg_for(int(kind[5:]), seed, False, g))
         if kind.startswith("sd"):
-            return pk.decode_sd(draft, target_full, prompts[i], cfg_for(int(kind[2:]), seed, False, g))
+            return pk.decode_sd(draft_full, target_full, prompts[i], cfg_for(int(kind[2:]), seed, False, g))
         return pk.decode_autoregressive(target_full, prompts[i], cfg_for(1, seed, False, g))
 
     def leg(kind, g=greedy, clocks=False):
@@ -267,7 +272,7 @@ def run_gpu(args):
     summary = run_summaries(target, draft, timed, args)
     split_model = split_pair_model(target, draft, results["pearl"]["alpha"]) if ws == 1 else None
     target_bytes, draft_bytes = target.cfg.weight_bytes(), draft.cfg.weight_bytes()
-    sweep = batch_sweep(target_full, draft, args, sweep_bs, greedy, temp, ws) if sweep_bs else None
+    sweep = batch_sweep(target_full, draft_full, args, sweep_bs, greedy, temp, ws) if sweep_bs else None
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(target, draft, prompts[0], args, greedy, temp)
@@ -300,7 +305,7 @@ def run_gpu(args):
             "adaptive_gamma": True, "gamma_max": args.gamma_max,
             "planner_calibration": cal.source, "temperature": 0.0 if greedy else temp,
             "target_gemm": args.gemm_target, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-            "draft_sms": draft_sms_used, "ar_sd_target": "whole GPU (own stream-K grids)",
+            "draft_sms": draft_sms_used, "ar_sd_target": "whole GPU (own stream-K grids, target and tcgen05 draft)",
             "l2": f"weights {wbytes / 1e9:.2f} GB vs 126 MB L2: "
                   + ("every forward streams HBM (no flush needed)" if wbytes > 126e6 else "L2-resident (tiny pair)"),
         },

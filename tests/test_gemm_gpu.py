@@ -18,9 +18,9 @@ def lib():
     return _lib
 
 
-def _gemm(lib, kind, W, X, splits=0):
+def _gemm(lib, kind, W, X, splits=0, N=None):
     M, K = X.shape
-    N = W.shape[0]
+    N = W.shape[0] if N is None else N
     Y = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
     lib.check(lib.load().pearl_gemm(kind, W.data_ptr(), X.data_ptr(), Y.data_ptr(), M, N, K, splits,
                                     torch.cuda.current_stream().cuda_stream), "pearl_gemm")
@@ -66,3 +66,16 @@ def test_split_k_is_deterministic_and_close(lib):
     assert torch.equal(a, _gemm(lib, 1, W, X))
     b = _gemm(lib, 1, W, X, splits=1)
     assert (a - b).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("N,K", [(4096, 4096), (22016, 4096), (4096, 11008)])
+def test_tile_major_weights_bitwise(lib, N, K):
+    """PEARL_GEMM_W_TILED: the same weights stored tile-major ([N/128][K/64]
+    [128][64], every TMA box one contiguous 16 KB) give bitwise the row-major
+    result for decode and prefill windows."""
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    W = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    Wt = W.view(N // 128, 128, K // 64, 64).permute(0, 2, 1, 3).contiguous()
+    for M in (1, 16, 20, 64, 128):
+        X = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+        assert torch.equal(_gemm(lib, 1, W, X), _gemm(lib, 1 | 0x100, Wt, X, N=N)), (N, K, M)
