@@ -834,7 +834,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pair", default="llama2-7b/68m")
     ap.add_argument("--gamma", type=int, default=4, help="initial draft length of adaptive PEARL")
-    ap.add_argument("--sd-gammas", default="4,8,16", help="fixed draft lengths of the vanilla SD legs")
+    ap.add_argument("--sd-gammas", default="4,8,16,20,24,32", help="fixed draft lengths of the vanilla SD legs (the best of them is the SD baseline)")
     ap.add_argument("--pearl-gammas", default="4,8,16,24", help="fixed draft lengths of the fixed-gamma PEARL legs")
     ap.add_argument("--gamma-max", type=int, default=32)
     ap.add_argument("--prompt", type=int, default=128)
