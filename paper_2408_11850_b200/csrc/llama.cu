@@ -228,6 +228,14 @@ struct GemvNorm {
   const float* xh;  // [M, K] fp32 residual stream, or nullptr (X is bf16 input)
   const float* g;   // [K] gain
   float eps;
+  // gemv1_kernel only (single token, layer 0 of a CUDA-core model): the row
+  // is the embedding of *tok (bf16 -> fp32 is exact, so rs and the operand are
+  // bitwise those of the embed kernel's h), and block 0 also writes it to
+  // h_out -- the embedding kernel folded into the first QKV GEMV.
+  const bf16* emb = nullptr;
+  const int32_t* tok = nullptr;
+  int V = 0;
+  float* h_out = nullptr;
 };
 
 constexpr int kGemvMaxNormTok = 64;
@@ -382,22 +390,350 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const bf16* __res
   gemv_block<TOK, RPW>(W, X, M, N, K, e, nrm, blockIdx.x, s_rs, s_out);
 }
 
+// Single-token K2 (M = 1, K <= kGemv1MaxK): gemv_block<1, RPW>'s per-row
+// arithmetic exactly (chunk k = 256 c + 8 lane, FMA order, xor tree, operand
+// rounding), restructured for memory-level parallelism.  gemv_block's chunk
+// loop issues one chunk's loads, branches, and FMAs them before the next
+// chunk's loads (one DRAM round trip per chunk: 12 for the 68M down
+// projection); here a warp requests CB chunks of all its rows before using
+// any -- the first batch BEFORE the PDL wait, since weights never depend on
+// the previous kernel -- and the operand row (bf16 X, or the fused-norm
+// bf16(h * rs * g)) is staged once per block in shared memory.
+constexpr int kGemv1MaxK = 4096;
+
+// Four consecutive row values as fp32: the fp32 residual row, or (bf16 row)
+// the embedding row widened exactly.
+__device__ __forceinline__ float4 row4(const float* xh, const bf16* eb, int j4) {
+  if (eb == nullptr) return reinterpret_cast<const float4*>(xh)[j4];
+  const uint2 u = *reinterpret_cast<const uint2*>(eb + 4 * j4);
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u), __uint_as_float(u.y << 16),
+                     __uint_as_float(u.y & 0xffff0000u));
+}
+
+// rs = 1 / sqrt(mean(row^2) + eps) of one row, in gemv_block's order
+// (lane l: float4 elements l + 32 u, 8 in flight per pass; xor tree)
+__device__ __forceinline__ float gemv_row_rs(const float* xh, const bf16* eb, int K, float eps, int lane) {
+  float ss = 0.f;
+  for (int j0 = lane; j0 < K / 4; j0 += 32 * 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + 32 * u;
+      v[u] = j < K / 4 ? row4(xh, eb, j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (j0 + 32 * u < K / 4) {
+        ss = fmaf(v[u].x, v[u].x, ss);
+        ss = fmaf(v[u].y, v[u].y, ss);
+        ss = fmaf(v[u].z, v[u].z, ss);
+        ss = fmaf(v[u].w, v[u].w, ss);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  return 1.0f / sqrtf(ss / static_cast<float>(K) + eps);
+}
+
+// residency: at least 6 blocks per SM for the short single-batch rows (the
+// 68M draft's qkv / gate_up grids in one wave), 3 for 4-row warps, 2 for CB = 12
+// and the embedding-fold variants (one launch per token: no spills)
+template <int RPW, int CB, bool EMB>
+constexpr int gemv1_min_blocks() { return (EMB || CB >= 12) ? 2 : (RPW == 4 ? 3 : 6); }
+
+template <int RPW, int CB, bool EMB = false>
+__global__ void __launch_bounds__(kGemvWarps * 32, gemv1_min_blocks<RPW, CB, EMB>()) gemv1_kernel(const bf16* __restrict__ W,
+                                                                const bf16* __restrict__ X, int N, int K, EpiArgs e,
+                                                                GemvNorm nrm) {
+  __shared__ __align__(16) bf16 s_x[kGemv1MaxK];
+  __shared__ float s_rs;
+  __shared__ float s_out[RPW == 1 ? kGemvWarps : 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = (blockIdx.x * kGemvWarps + warp) * RPW;
+  const bool active = n0 < N;
+  const int nchunk = (K + 255) / 256;
+  uint4 wr[CB][RPW];
+  auto issue = [&](int c0) {
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      const int k = (c0 + u) * 256 + lane * 8;
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const int n = min(n0 + r, N - 1);
+        wr[u][r] = (active && k < K) ? ld_nc_v4(W + static_cast<size_t>(n) * K + k) : make_uint4(0, 0, 0, 0);
+      }
+    }
+  };
+  issue(0);
+  pdl_wait();
+  pdl_trigger();
+  if (e.adv_pos != nullptr && blockIdx.x == 0 && tid == 0) *e.adv_pos += e.adv_n;
+  if (EMB || nrm.xh != nullptr) {
+    const bf16* eb = nullptr;
+    if (EMB) {
+      int tok = *nrm.tok;
+      tok = tok < 0 ? 0 : (tok >= nrm.V ? nrm.V - 1 : tok);
+      eb = nrm.emb + static_cast<size_t>(tok) * K;
+    }
+    if (warp == 0) {
+      const float rs = gemv_row_rs(nrm.xh, eb, K, nrm.eps, lane);
+      if (lane == 0) s_rs = rs;
+    }
+    __syncthreads();
+    const float rs = s_rs;
+    for (int k = tid * 4; k < K; k += kGemvWarps * 32 * 4) {
+      const float4 h4 = row4(nrm.xh, eb, k / 4);
+      if (EMB && blockIdx.x == 0) *reinterpret_cast<float4*>(nrm.h_out + k) = h4;
+      const float4 g4 = *reinterpret_cast<const float4*>(nrm.g + k);
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(h4.x * rs * g4.x, h4.y * rs * g4.y);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(h4.z * rs * g4.z, h4.w * rs * g4.w);
+      *reinterpret_cast<uint2*>(s_x + k) =
+          make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    }
+  } else {
+    for (int k = tid * 8; k < K; k += kGemvWarps * 32 * 8)
+      *reinterpret_cast<uint4*>(s_x + k) = __ldg(reinterpret_cast<const uint4*>(X + k));
+  }
+  __syncthreads();
+  float acc[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) acc[r] = 0.f;
+  for (int c0 = 0; c0 < nchunk; c0 += CB) {
+    if (c0 > 0) issue(c0);
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      const int k = (c0 + u) * 256 + lane * 8;
+      if (active && k < K) {
+        float xv[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(s_x + k), xv);
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          float w[8];
+          bf16x8_to_f32(wr[u][r], w);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[r] = fmaf(w[j], xv[j], acc[r]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+  if (RPW == 4) {
+    if (active && lane == 0) {
+      float v[4] = {acc[0], acc[1 % RPW], acc[2 % RPW], acc[3 % RPW]};
+      epilogue4(e, 0, n0, v, N);
+    }
+  } else {
+    if (lane == 0) s_out[warp] = acc[0];
+    __syncthreads();
+    const int nq = blockIdx.x * kGemvWarps + 4 * tid;
+    if (tid < kGemvWarps / 4 && nq < N) {
+      float v[4] = {s_out[4 * tid], s_out[4 * tid + 1], s_out[4 * tid + 2], s_out[4 * tid + 3]};
+      epilogue4(e, 0, nq, v, N);
+    }
+  }
+}
+
+// Single-token K2, bulk-copy streamed (K2s): the same per-row arithmetic as
+// gemv_block / gemv1_kernel, with the weights moved by the bulk-copy engine.
+// Work = 4-row groups (4 consecutive rows = one contiguous 8K-byte range of
+// W); warp gw of the persistent grid (one CTA per SM of the model's SMs)
+// takes groups gw, gw + G, ...  Each warp owns a D-deep ring of 4-row slots
+// in shared memory: lane 0 requests a group with one cp.async.bulk
+// (mbarrier completion) and re-requests the next as soon as the warp has read
+// a slot, so a warp keeps D groups in flight with no registers held -- the
+// first D before the PDL wait.  Up to ~190 KB per SM is in flight, which is
+// what a partition of a few dozen SMs needs to stream at its share of HBM
+// (the register-held loads of gemv1_kernel cap an SM at ~60-100 KB).
+constexpr int kGemvsWarps = 8;
+constexpr int kGemvsRingBytes = 24 * 1024;  // per warp
+constexpr int kGemvsMaxD = 8;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+size_t gemvs_smem(int K) { return static_cast<size_t>(kGemvsWarps) * kGemvsRingBytes + static_cast<size_t>(K) * 2 + 16; }
+
+template <bool EMB>
+__global__ void __launch_bounds__(kGemvsWarps * 32, 1) gemvs_kernel(const bf16* __restrict__ W,
+                                                                   const bf16* __restrict__ X, int N, int K, EpiArgs e,
+                                                                   GemvNorm nrm) {
+  extern __shared__ __align__(128) unsigned char gs_raw[];
+  __shared__ __align__(8) uint64_t s_full[kGemvsWarps][kGemvsMaxD];
+  __shared__ float s_rs;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int slot_bytes = 4 * K * 2;
+  const int D = min(kGemvsMaxD, kGemvsRingBytes / slot_bytes);  // host guarantees D >= 1
+  unsigned char* ring = gs_raw + static_cast<size_t>(warp) * kGemvsRingBytes;
+  bf16* s_x = reinterpret_cast<bf16*>(gs_raw + static_cast<size_t>(kGemvsWarps) * kGemvsRingBytes);
+  const int ngroups = (N + 3) / 4;
+  const int G = gridDim.x * kGemvsWarps;
+  const int gw = blockIdx.x * kGemvsWarps + warp;
+  auto request = [&](int i, int g) {  // lane 0: group g into slot i
+    const int rows = min(4, N - 4 * g);
+    const uint32_t bytes = static_cast<uint32_t>(rows) * K * 2;
+    mbar_expect_tx(&s_full[warp][i], bytes);
+    bulk_g2s(ring + static_cast<size_t>(i) * slot_bytes, W + static_cast<size_t>(4 * g) * K, bytes, &s_full[warp][i]);
+  };
+  if (lane == 0) {
+    for (int i = 0; i < D; ++i) mbar_init(&s_full[warp][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < D && gw + i * G < ngroups; ++i) request(i, gw + i * G);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (e.adv_pos != nullptr && blockIdx.x == 0 && tid == 0) *e.adv_pos += e.adv_n;
+  // operand row, exactly as gemv1_kernel stages it
+  if (EMB || nrm.xh != nullptr) {
+    const bf16* eb = nullptr;
+    if (EMB) {
+      int tok = *nrm.tok;
+      tok = tok < 0 ? 0 : (tok >= nrm.V ? nrm.V - 1 : tok);
+      eb = nrm.emb + static_cast<size_t>(tok) * K;
+    }
+    if (warp == 0) {
+      const float rs = gemv_row_rs(nrm.xh, eb, K, nrm.eps, lane);
+      if (lane == 0) s_rs = rs;
+    }
+    __syncthreads();
+    const float rs = s_rs;
+    for (int k = tid * 4; k < K; k += kGemvsWarps * 32 * 4) {
+      const float4 h4 = row4(nrm.xh, eb, k / 4);
+      if (EMB && blockIdx.x == 0) *reinterpret_cast<float4*>(nrm.h_out + k) = h4;
+      const float4 g4 = *reinterpret_cast<const float4*>(nrm.g + k);
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(h4.x * rs * g4.x, h4.y * rs * g4.y);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(h4.z * rs * g4.z, h4.w * rs * g4.w);
+      *reinterpret_cast<uint2*>(s_x + k) =
+          make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    }
+  } else {
+    for (int k = tid * 8; k < K; k += kGemvsWarps * 32 * 8)
+      *reinterpret_cast<uint4*>(s_x + k) = __ldg(reinterpret_cast<const uint4*>(X + k));
+  }
+  __syncthreads();
+  const int nchunk = (K + 255) / 256;
+  uint32_t phase = 0;  // bit i: parity of slot i's next completion
+  int i = 0;
+  for (int g = gw; g < ngroups; g += G) {
+    mbar_wait(&s_full[warp][i], (phase >> i) & 1u);
+    phase ^= 1u << i;
+    const bf16* sw = reinterpret_cast<const bf16*>(ring + static_cast<size_t>(i) * slot_bytes);
+    const int rows = min(4, N - 4 * g);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < nchunk; ++c) {
+      const int k = c * 256 + lane * 8;
+      if (k < K) {
+        float xv[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(s_x + k), xv);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < rows) {
+            float w[8];
+            bf16x8_to_f32(*reinterpret_cast<const uint4*>(sw + static_cast<size_t>(r) * K + k), w);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[r] = fmaf(w[j], xv[j], acc[r]);
+          }
+        }
+      }
+    }
+    // the slot is free once every lane has read it: re-request (async proxy
+    // write after generic reads -> proxy fence)
+    __syncwarp();
+    if (lane == 0 && g + D * G < ngroups) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      request(i, g + D * G);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+    if (lane == 0) epilogue4(e, 0, 4 * g, acc, N);
+    i = (i + 1 == D) ? 0 : i + 1;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 namespace {
 
+// PEARL_GEMV1=0 restores gemv_kernel<1, RPW> for single tokens (A/B diagnostics;
+// bitwise the same results)
+static bool gemv1_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PEARL_GEMV1");
+    return !(v && std::atoi(v) == 0);
+  }();
+  return on;
+}
+
+// PEARL_GEMVS=0 disables the bulk-copy streamed single-token GEMV (K2s)
+static bool gemvs_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PEARL_GEMVS");
+    return !(v && std::atoi(v) == 0);
+  }();
+  return on;
+}
+
+static int device_sms() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+constexpr int kGemvsMaxK = kGemvsRingBytes / 8;  // one 4-row slot per warp at least
+
+int launch_gemvs(const bf16* W, const bf16* X, int N, int K, const EpiArgs& e, cudaStream_t st, const GemvNorm& nrm,
+                 int sms) {
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] {
+    const int bytes = static_cast<int>(gemvs_smem(kGemvsMaxK));
+    attr_rc = cudaFuncSetAttribute(gemvs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ||
+              cudaFuncSetAttribute(gemvs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  });
+  if (attr_rc) return PEARL_ERR_CUDA;
+  const int ngroups = (N + 3) / 4;
+  const int grid = std::max(1, std::min(sms > 0 ? sms : device_sms(), (ngroups + kGemvsWarps - 1) / kGemvsWarps));
+  const size_t smem = gemvs_smem(K);
+  if (nrm.emb != nullptr)
+    return launch_pdl(gemvs_kernel<true>, dim3(grid), dim3(kGemvsWarps * 32), smem, st, W, X, N, K, e, nrm);
+  return launch_pdl(gemvs_kernel<false>, dim3(grid), dim3(kGemvsWarps * 32), smem, st, W, X, N, K, e, nrm);
+}
+
 int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
-                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
+                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}, int sms = 0) {
+  if (M == 1 && K <= kGemvsMaxK && K % 8 == 0 && gemv1_enabled() && gemvs_enabled())
+    return launch_gemvs(W, X, N, K, e, st, nrm, sms);
   // narrow layers: one row per warp (4x the warps; same per-row arithmetic)
   const bool narrow = (N + kGemvWarps * kGemvRows - 1) / (kGemvWarps * kGemvRows) < 296;
   const dim3 block(kGemvWarps * 32);
+  const bool m1 = M == 1 && K <= kGemv1MaxK && gemv1_enabled();
+  const int nchunk = (K + 255) / 256;
   if (narrow) {
     const dim3 grid((N + kGemvWarps - 1) / kGemvWarps);
+    if (m1 && nrm.emb != nullptr && nchunk <= 4)
+      return launch_pdl(gemv1_kernel<1, 4, true>, grid, block, 0, st, W, X, N, K, e, nrm);
+    if (m1 && nrm.emb != nullptr) return launch_pdl(gemv1_kernel<1, 12, true>, grid, block, 0, st, W, X, N, K, e, nrm);
+    if (m1 && nchunk <= 4) return launch_pdl(gemv1_kernel<1, 4>, grid, block, 0, st, W, X, N, K, e, nrm);
+    if (m1) return launch_pdl(gemv1_kernel<1, 12>, grid, block, 0, st, W, X, N, K, e, nrm);
     if (M == 1) return launch_pdl(gemv_kernel<1, 1>, grid, block, 0, st, W, X, M, N, K, e, nrm);
     return launch_pdl(gemv_kernel<8, 1>, grid, block, 0, st, W, X, M, N, K, e, nrm);
   }
   const dim3 grid((N + kGemvWarps * kGemvRows - 1) / (kGemvWarps * kGemvRows));
+  if (m1 && nrm.emb != nullptr) return launch_pdl(gemv1_kernel<4, 3, true>, grid, block, 0, st, W, X, N, K, e, nrm);
+  if (m1) return launch_pdl(gemv1_kernel<4, 3>, grid, block, 0, st, W, X, N, K, e, nrm);
   if (M == 1) return launch_pdl(gemv_kernel<1, 4>, grid, block, 0, st, W, X, M, N, K, e, nrm);
   return launch_pdl(gemv_kernel<8, 4>, grid, block, 0, st, W, X, M, N, K, e, nrm);
 }
@@ -407,7 +743,7 @@ int launch_gemm(Llama& m, const bf16* W, const bf16* X, int M, int N, int K, con
                 GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
   if (ablate_mask() & 4) return PEARL_OK;
   if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st, 0);
-  return launch_gemv(W, X, M, N, K, e, st, nrm);
+  return launch_gemv(W, X, M, N, K, e, st, nrm, m.num_sms);
 }
 
 // Diagnostics only (PEARL_ABLATE=attn|gemm): skip a kernel class to
@@ -463,10 +799,16 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     e.norm_d = d;
     e.norm_eps = c.norm_eps;
   };
-  int rc = launch_pdl(embed_kernel, dim3(M), dim3(kEmbedThreads), 0, st, tokens, m.embed, m.h, d, c.vocab,
-                      fold ? m.layers[0].attn_norm : static_cast<const float*>(nullptr),
-                      fold ? m.x : static_cast<bf16*>(nullptr), m.ss, T);
-  if (rc) return rc;
+  // single-token CUDA-core forwards fold the embedding into layer 0's QKV
+  // GEMV (gemv1_kernel reads the embedding row and writes h)
+  const bool embed_fold = fuse_norm && M == 1 && d <= kGemv1MaxK && gemv1_enabled() && stop < 0 && abl == 0;
+  int rc = PEARL_OK;
+  if (!embed_fold) {
+    rc = launch_pdl(embed_kernel, dim3(M), dim3(kEmbedThreads), 0, st, tokens, m.embed, m.h, d, c.vocab,
+                    fold ? m.layers[0].attn_norm : static_cast<const float*>(nullptr),
+                    fold ? m.x : static_cast<bf16*>(nullptr), m.ss, T);
+    if (rc) return rc;
+  }
   g_prof.mark(OP_EMBED, st);
   if (halt()) return PEARL_OK;
   const size_t slot_kv = static_cast<size_t>(c.max_seq) * nkv;
@@ -491,8 +833,15 @@ int forward_chunk(Llama& m, const int32_t* tokens, int M, int32_t* pos, int pos_
     e.n_kv = nkv;
     e.hd = hd;
     consume(e, 0);
-    rc = launch_gemm(m, Lw.wqkv, m.x, M, nq + 2 * nkv, d, e, st,
-                     fuse_norm ? GemvNorm{m.h, Lw.attn_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f});
+    GemvNorm qn = fuse_norm ? GemvNorm{m.h, Lw.attn_norm, c.norm_eps} : GemvNorm{nullptr, nullptr, 0.f};
+    if (embed_fold && l == 0) {
+      qn.xh = nullptr;
+      qn.emb = m.embed;
+      qn.tok = tokens;
+      qn.V = c.vocab;
+      qn.h_out = m.h;
+    }
+    rc = launch_gemm(m, Lw.wqkv, m.x, M, nq + 2 * nkv, d, e, st, qn);
     if (rc) return rc;
     g_prof.mark(OP_QKV, st);
     if (halt()) return PEARL_OK;
