@@ -674,11 +674,11 @@ static bool gemv1_enabled() {
   return on;
 }
 
-// PEARL_GEMVS=0 disables the bulk-copy streamed single-token GEMV (K2s)
+// PEARL_GEMVS=1 enables the bulk-copy streamed single-token GEMV (K2s)
 static bool gemvs_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("PEARL_GEMVS");
-    return !(v && std::atoi(v) == 0);
+    return v && std::atoi(v) == 1;
   }();
   return on;
 }
