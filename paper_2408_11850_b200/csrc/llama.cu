@@ -537,128 +537,6 @@ __global__ void __launch_bounds__(kGemvWarps * 32, gemv1_min_blocks<RPW, CB, EMB
   }
 }
 
-// Single-token K2, bulk-copy streamed (K2s): the same per-row arithmetic as
-// gemv_block / gemv1_kernel, with the weights moved by the bulk-copy engine.
-// Work = 4-row groups (4 consecutive rows = one contiguous 8K-byte range of
-// W); warp gw of the persistent grid (one CTA per SM of the model's SMs)
-// takes groups gw, gw + G, ...  Each warp owns a D-deep ring of 4-row slots
-// in shared memory: lane 0 requests a group with one cp.async.bulk
-// (mbarrier completion) and re-requests the next as soon as the warp has read
-// a slot, so a warp keeps D groups in flight with no registers held -- the
-// first D before the PDL wait.  Up to ~190 KB per SM is in flight, which is
-// what a partition of a few dozen SMs needs to stream at its share of HBM
-// (the register-held loads of gemv1_kernel cap an SM at ~60-100 KB).
-constexpr int kGemvsWarps = 8;
-constexpr int kGemvsRingBytes = 24 * 1024;  // per warp
-constexpr int kGemvsMaxD = 8;
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-size_t gemvs_smem(int K) { return static_cast<size_t>(kGemvsWarps) * kGemvsRingBytes + static_cast<size_t>(K) * 2 + 16; }
-
-template <bool EMB>
-__global__ void __launch_bounds__(kGemvsWarps * 32, 1) gemvs_kernel(const bf16* __restrict__ W,
-                                                                   const bf16* __restrict__ X, int N, int K, EpiArgs e,
-                                                                   GemvNorm nrm) {
-  extern __shared__ __align__(128) unsigned char gs_raw[];
-  __shared__ __align__(8) uint64_t s_full[kGemvsWarps][kGemvsMaxD];
-  __shared__ float s_rs;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int slot_bytes = 4 * K * 2;
-  const int D = min(kGemvsMaxD, kGemvsRingBytes / slot_bytes);  // host guarantees D >= 1
-  unsigned char* ring = gs_raw + static_cast<size_t>(warp) * kGemvsRingBytes;
-  bf16* s_x = reinterpret_cast<bf16*>(gs_raw + static_cast<size_t>(kGemvsWarps) * kGemvsRingBytes);
-  const int ngroups = (N + 3) / 4;
-  const int G = gridDim.x * kGemvsWarps;
-  const int gw = blockIdx.x * kGemvsWarps + warp;
-  auto request = [&](int i, int g) {  // lane 0: group g into slot i
-    const int rows = min(4, N - 4 * g);
-    const uint32_t bytes = static_cast<uint32_t>(rows) * K * 2;
-    mbar_expect_tx(&s_full[warp][i], bytes);
-    bulk_g2s(ring + static_cast<size_t>(i) * slot_bytes, W + static_cast<size_t>(4 * g) * K, bytes, &s_full[warp][i]);
-  };
-  if (lane == 0) {
-    for (int i = 0; i < D; ++i) mbar_init(&s_full[warp][i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int i = 0; i < D && gw + i * G < ngroups; ++i) request(i, gw + i * G);
-  }
-  pdl_wait();
-  pdl_trigger();
-  if (e.adv_pos != nullptr && blockIdx.x == 0 && tid == 0) *e.adv_pos += e.adv_n;
-  // operand row, exactly as gemv1_kernel stages it
-  if (EMB || nrm.xh != nullptr) {
-    const bf16* eb = nullptr;
-    if (EMB) {
-      int tok = *nrm.tok;
-      tok = tok < 0 ? 0 : (tok >= nrm.V ? nrm.V - 1 : tok);
-      eb = nrm.emb + static_cast<size_t>(tok) * K;
-    }
-    if (warp == 0) {
-      const float rs = gemv_row_rs(nrm.xh, eb, K, nrm.eps, lane);
-      if (lane == 0) s_rs = rs;
-    }
-    __syncthreads();
-    const float rs = s_rs;
-    for (int k = tid * 4; k < K; k += kGemvsWarps * 32 * 4) {
-      const float4 h4 = row4(nrm.xh, eb, k / 4);
-      if (EMB && blockIdx.x == 0) *reinterpret_cast<float4*>(nrm.h_out + k) = h4;
-      const float4 g4 = *reinterpret_cast<const float4*>(nrm.g + k);
-      const __nv_bfloat162 lo = __floats2bfloat162_rn(h4.x * rs * g4.x, h4.y * rs * g4.y);
-      const __nv_bfloat162 hi = __floats2bfloat162_rn(h4.z * rs * g4.z, h4.w * rs * g4.w);
-      *reinterpret_cast<uint2*>(s_x + k) =
-          make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
-    }
-  } else {
-    for (int k = tid * 8; k < K; k += kGemvsWarps * 32 * 8)
-      *reinterpret_cast<uint4*>(s_x + k) = __ldg(reinterpret_cast<const uint4*>(X + k));
-  }
-  __syncthreads();
-  const int nchunk = (K + 255) / 256;
-  uint32_t phase = 0;  // bit i: parity of slot i's next completion
-  int i = 0;
-  for (int g = gw; g < ngroups; g += G) {
-    mbar_wait(&s_full[warp][i], (phase >> i) & 1u);
-    phase ^= 1u << i;
-    const bf16* sw = reinterpret_cast<const bf16*>(ring + static_cast<size_t>(i) * slot_bytes);
-    const int rows = min(4, N - 4 * g);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int c = 0; c < nchunk; ++c) {
-      const int k = c * 256 + lane * 8;
-      if (k < K) {
-        float xv[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(s_x + k), xv);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          if (r < rows) {
-            float w[8];
-            bf16x8_to_f32(*reinterpret_cast<const uint4*>(sw + static_cast<size_t>(r) * K + k), w);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[r] = fmaf(w[j], xv[j], acc[r]);
-          }
-        }
-      }
-    }
-    // the slot is free once every lane has read it: re-request (async proxy
-    // write after generic reads -> proxy fence)
-    __syncwarp();
-    if (lane == 0 && g + D * G < ngroups) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      request(i, g + D * G);
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
-    if (lane == 0) epilogue4(e, 0, 4 * g, acc, N);
-    i = (i + 1 == D) ? 0 : i + 1;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -674,48 +552,8 @@ static bool gemv1_enabled() {
   return on;
 }
 
-// PEARL_GEMVS=1 enables the bulk-copy streamed single-token GEMV (K2s)
-static bool gemvs_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("PEARL_GEMVS");
-    return v && std::atoi(v) == 1;
-  }();
-  return on;
-}
-
-static int device_sms() {
-  static const int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
-
-constexpr int kGemvsMaxK = kGemvsRingBytes / 8;  // one 4-row slot per warp at least
-
-int launch_gemvs(const bf16* W, const bf16* X, int N, int K, const EpiArgs& e, cudaStream_t st, const GemvNorm& nrm,
-                 int sms) {
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] {
-    const int bytes = static_cast<int>(gemvs_smem(kGemvsMaxK));
-    attr_rc = cudaFuncSetAttribute(gemvs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ||
-              cudaFuncSetAttribute(gemvs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  });
-  if (attr_rc) return PEARL_ERR_CUDA;
-  const int ngroups = (N + 3) / 4;
-  const int grid = std::max(1, std::min(sms > 0 ? sms : device_sms(), (ngroups + kGemvsWarps - 1) / kGemvsWarps));
-  const size_t smem = gemvs_smem(K);
-  if (nrm.emb != nullptr)
-    return launch_pdl(gemvs_kernel<true>, dim3(grid), dim3(kGemvsWarps * 32), smem, st, W, X, N, K, e, nrm);
-  return launch_pdl(gemvs_kernel<false>, dim3(grid), dim3(kGemvsWarps * 32), smem, st, W, X, N, K, e, nrm);
-}
-
 int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
-                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}, int sms = 0) {
-  if (M == 1 && K <= kGemvsMaxK && K % 8 == 0 && gemv1_enabled() && gemvs_enabled())
-    return launch_gemvs(W, X, N, K, e, st, nrm, sms);
+                GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
   // narrow layers: one row per warp (4x the warps; same per-row arithmetic)
   const bool narrow = (N + kGemvWarps * kGemvRows - 1) / (kGemvWarps * kGemvRows) < 296;
   const dim3 block(kGemvWarps * 32);
@@ -743,7 +581,7 @@ int launch_gemm(Llama& m, const bf16* W, const bf16* X, int M, int N, int K, con
                 GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
   if (ablate_mask() & 4) return PEARL_OK;
   if (m.cfg.gemm_kind == PEARL_GEMM_TCGEN05) return tc_gemm(m.tc, W, X, M, N, K, e, st, 0);
-  return launch_gemv(W, X, M, N, K, e, st, nrm, m.num_sms);
+  return launch_gemv(W, X, M, N, K, e, st, nrm);
 }
 
 // Diagnostics only (PEARL_ABLATE=attn|gemm): skip a kernel class to
