@@ -256,8 +256,10 @@ def run_gpu(args):
         clocks = ck or clocks
     greedy_leg = None
     if args.greedy_leg and not greedy:
-        # BASELINE configs[1]: temperature 0 as well (greedy device path); the
-        # planner keeps the same frozen step-time table
+        # BASELINE configs[1]: temperature 0 as well (greedy device path), with
+        # the pair's T=0 planner table (committed, or measured under
+        # --live-calibration): alpha-hat 1 prices long draft blocks differently
+        planner_calibration(draft, target, args, prompts[0], True, temp)
         g_res = {}
         for kind in ["ar"] + [f"sd{g}" for g in sd_gammas] + ["pearl"]:
             g_res[kind] = leg(kind, g=True)[0]
