@@ -45,7 +45,13 @@ def test_matches_fp32_reference(lib, kind, N, K):
 @pytest.mark.parametrize("kind", [0, 1])
 def test_batch_invariance(lib, kind):
     g = torch.Generator(device="cuda").manual_seed(5)
-    for N, K in [(4096, 4096), (300, 1376), (32000, 768)]:
+    shapes = [(4096, 4096), (300, 1376), (32000, 768)]
+    if kind == 0:
+        # K2's single-token kernel (gemv1_kernel): one chunk batch (768 / 3072: the
+        # 68M draft's o / down), a 12 + 1 chunk split (3328), ragged N and K, the
+        # 4-row-per-warp wide path (9999 rows) -- all bitwise the multi-token rows
+        shapes += [(768, 3072), (1001, 3328), (9999, 520), (2304, 768)]
+    for N, K in shapes:
         W = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
         X = torch.randn(128, K, generator=g, device="cuda").to(torch.bfloat16)
         full = _gemm(lib, kind, W, X)
