@@ -436,6 +436,110 @@ __device__ __forceinline__ float gemv_row_rs(const float* xh, const bf16* eb, in
   return 1.0f / sqrtf(ss / static_cast<float>(K) + eps);
 }
 
+// Single-token fused-norm GEMV with the RMS scale in registers (K = 128 NV:
+// the 68M draft's QKV / gate-up, d = 768).  gemv1_kernel stages the operand
+// through smem: warp 0 computes rs (one L2 round trip), block barrier, every
+// thread builds bf16(h * rs * g) (a second round trip), block barrier.  Here
+// every warp loads the whole row once in gemv_row_rs's own layout (lane l:
+// float4 elements l + 32 u), computes rs itself in that order, and gathers the
+// h values of its lanes' chunks with shuffles -- one round trip after the PDL
+// wait and no block barrier; g is staged in smem before the wait.  4 rows per
+// warp, every chunk of a row in flight at once.  Bitwise gemv_block's rows.
+template <int NV, bool EMB>
+__global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv1n_kernel(const bf16* __restrict__ W, int N, EpiArgs e,
+                                                                    GemvNorm nrm) {
+  constexpr int K = 128 * NV;
+  constexpr int NC = NV / 2;  // 256-element chunks
+  __shared__ __align__(16) float s_g[K];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = (blockIdx.x * kGemvWarps + warp) * 4;
+  const bool active = n0 < N;
+  uint4 wr[NC][4];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int n = min(n0 + r, N - 1);
+      wr[c][r] = active ? ld_nc_v4(W + static_cast<size_t>(n) * K + c * 256 + lane * 8) : make_uint4(0, 0, 0, 0);
+    }
+  for (int k = tid * 4; k < K; k += kGemvWarps * 32 * 4)
+    *reinterpret_cast<float4*>(s_g + k) = *reinterpret_cast<const float4*>(nrm.g + k);
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (e.adv_pos != nullptr && blockIdx.x == 0 && tid == 0) *e.adv_pos += e.adv_n;
+  const bf16* eb = nullptr;
+  if (EMB) {
+    int tok = *nrm.tok;
+    tok = tok < 0 ? 0 : (tok >= nrm.V ? nrm.V - 1 : tok);
+    eb = nrm.emb + static_cast<size_t>(tok) * K;
+  }
+  float4 v[NV];
+#pragma unroll
+  for (int u = 0; u < NV; ++u) v[u] = row4(nrm.xh, eb, lane + 32 * u);
+  if (EMB && blockIdx.x == 0 && warp == 0)
+#pragma unroll
+    for (int u = 0; u < NV; ++u) *reinterpret_cast<float4*>(nrm.h_out + 4 * (lane + 32 * u)) = v[u];
+  float ss = 0.f;  // gemv_row_rs: one pass of K / 4 <= 256 float4s, u order
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    ss = fmaf(v[u].x, v[u].x, ss);
+    ss = fmaf(v[u].y, v[u].y, ss);
+    ss = fmaf(v[u].z, v[u].z, ss);
+    ss = fmaf(v[u].w, v[u].w, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float rs = 1.0f / sqrtf(ss / static_cast<float>(K) + nrm.eps);
+  // chunk c of lane l covers float4 elements 64 c + 2 l and + 1: held by lanes
+  // (2 l) % 32 and (2 l + 1) % 32 in slot 2 c + (l >= 16)
+  const int srcA = (2 * lane) & 31, srcB = srcA + 1;
+  const bool hi = lane >= 16;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    float hv[8];
+    {
+      const float4 p = v[2 * c], q = v[2 * c + 1];
+      const float a0 = __shfl_sync(0xffffffffu, p.x, srcA), a1 = __shfl_sync(0xffffffffu, q.x, srcA);
+      const float b0 = __shfl_sync(0xffffffffu, p.y, srcA), b1 = __shfl_sync(0xffffffffu, q.y, srcA);
+      const float c0 = __shfl_sync(0xffffffffu, p.z, srcA), c1 = __shfl_sync(0xffffffffu, q.z, srcA);
+      const float d0 = __shfl_sync(0xffffffffu, p.w, srcA), d1 = __shfl_sync(0xffffffffu, q.w, srcA);
+      const float e0 = __shfl_sync(0xffffffffu, p.x, srcB), e1 = __shfl_sync(0xffffffffu, q.x, srcB);
+      const float f0 = __shfl_sync(0xffffffffu, p.y, srcB), f1 = __shfl_sync(0xffffffffu, q.y, srcB);
+      const float g0 = __shfl_sync(0xffffffffu, p.z, srcB), g1 = __shfl_sync(0xffffffffu, q.z, srcB);
+      const float h0 = __shfl_sync(0xffffffffu, p.w, srcB), h1 = __shfl_sync(0xffffffffu, q.w, srcB);
+      hv[0] = hi ? a1 : a0; hv[1] = hi ? b1 : b0; hv[2] = hi ? c1 : c0; hv[3] = hi ? d1 : d0;
+      hv[4] = hi ? e1 : e0; hv[5] = hi ? f1 : f0; hv[6] = hi ? g1 : g0; hv[7] = hi ? h1 : h0;
+    }
+    const int k = c * 256 + lane * 8;
+    const float4 g0 = *reinterpret_cast<const float4*>(s_g + k);
+    const float4 g1 = *reinterpret_cast<const float4*>(s_g + k + 4);
+    const float gk[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    float xv[8];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const __nv_bfloat162 b2 = __floats2bfloat162_rn(hv[j] * rs * gk[j], hv[j + 1] * rs * gk[j + 1]);
+      xv[j] = __low2float(b2);
+      xv[j + 1] = __high2float(b2);
+    }
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        float w[8];
+        bf16x8_to_f32(wr[c][r], w);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[r] = fmaf(w[j], xv[j], acc[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+  if (active && lane == 0) epilogue4(e, 0, n0, acc, N);
+}
+
 // residency: at least 6 blocks per SM for the short single-batch rows (the
 // 68M draft's qkv / gate_up grids in one wave), 3 for 4-row warps, 2 for CB = 12
 // and the embedding-fold variants (one launch per token: no spills)
@@ -552,8 +656,37 @@ static bool gemv1_enabled() {
   return on;
 }
 
+// PEARL_GEMV1N=0: fused-norm single-token GEMVs stage the operand through smem
+// (gemv1_kernel) instead of the register-norm gemv1n_kernel (A/B; bitwise equal)
+static bool gemv1n_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PEARL_GEMV1N");
+    return !(v && std::atoi(v) == 0);
+  }();
+  return on;
+}
+
+template <int NV>
+int launch_gemv1n(const bf16* W, int N, const EpiArgs& e, cudaStream_t st, const GemvNorm& nrm) {
+  const dim3 grid((N + kGemvWarps * 4 - 1) / (kGemvWarps * 4)), block(kGemvWarps * 32);
+  if (nrm.emb != nullptr) return launch_pdl(gemv1n_kernel<NV, true>, grid, block, 0, st, W, N, e, nrm);
+  return launch_pdl(gemv1n_kernel<NV, false>, grid, block, 0, st, W, N, e, nrm);
+}
+
 int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
                 GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
+  // single token, fused norm, d = 512 / 768 / 1024, not the lm_head (whose
+  // 1000+ blocks want gemv1_kernel's 3 blocks per SM)
+  static const bool head_n = [] {  // PEARL_GEMV1N_HEAD=1: the lm_head too (A/B)
+    const char* v = std::getenv("PEARL_GEMV1N_HEAD");
+    return v && std::atoi(v) == 1;
+  }();
+  if (M == 1 && (nrm.xh != nullptr || nrm.emb != nullptr) && (N <= 8192 || head_n) && gemv1_enabled() &&
+      gemv1n_enabled()) {
+    if (K == 512) return launch_gemv1n<4>(W, N, e, st, nrm);
+    if (K == 768) return launch_gemv1n<6>(W, N, e, st, nrm);
+    if (K == 1024) return launch_gemv1n<8>(W, N, e, st, nrm);
+  }
   // narrow layers: one row per warp (4x the warps; same per-row arithmetic)
   const bool narrow = (N + kGemvWarps * kGemvRows - 1) / (kGemvWarps * kGemvRows) < 296;
   const dim3 block(kGemvWarps * 32);
