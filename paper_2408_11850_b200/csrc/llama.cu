@@ -675,14 +675,10 @@ int launch_gemv1n(const bf16* W, int N, const EpiArgs& e, cudaStream_t st, const
 
 int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs& e, cudaStream_t st,
                 GemvNorm nrm = GemvNorm{nullptr, nullptr, 0.f}) {
-  // single token, fused norm, d = 512 / 768 / 1024, not the lm_head (whose
-  // 1000+ blocks want gemv1_kernel's 3 blocks per SM)
-  static const bool head_n = [] {  // PEARL_GEMV1N_HEAD=1: the lm_head too (A/B)
-    const char* v = std::getenv("PEARL_GEMV1N_HEAD");
-    return v && std::atoi(v) == 1;
-  }();
-  if (M == 1 && (nrm.xh != nullptr || nrm.emb != nullptr) && (N <= 8192 || head_n) && gemv1_enabled() &&
-      gemv1n_enabled()) {
+  // single token, fused norm, d = 512 / 768 / 1024, not the lm_head (its 1000
+  // blocks want gemv1_kernel's 3 per SM: gemv1n there measured 48.7 vs 49.2 us
+  // per 68M token on the whole GPU, and would run ~50 % more waves on a partition)
+  if (M == 1 && (nrm.xh != nullptr || nrm.emb != nullptr) && N <= 8192 && gemv1_enabled() && gemv1n_enabled()) {
     if (K == 512) return launch_gemv1n<4>(W, N, e, st, nrm);
     if (K == 768) return launch_gemv1n<6>(W, N, e, st, nrm);
     if (K == 1024) return launch_gemv1n<8>(W, N, e, st, nrm);
