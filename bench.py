@@ -670,9 +670,16 @@ def roofline(target, draft, gamma, args):
     c = target.cfg
     byts = _forward_bytes(c, M, ctx)
     achieved = byts / t / 1e9
-    tr = _traffic().get(f"{c.name}_M{M}")
+    # ncu DRAM bytes of one forward (profiles/traffic.json) at this window, else
+    # at the nearest captured window of this model (weights dominate: 7B M=16
+    # 13.53 GB, M=20 13.56 GB), named in traffic_window
+    tab = {k: v for k, v in _traffic().items() if k.startswith(f"{c.name}_M")}
+    tr, tr_m = None, None
+    if tab:
+        key = min(tab, key=lambda k: abs(int(k.rsplit("_M", 1)[1]) - M))
+        tr, tr_m = tab[key], int(key.rsplit("_M", 1)[1])
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": tr,
+            "frac": round(achieved / peak, 4), "traffic": tr, "traffic_window": tr_m,
             "kernel": f"target window forward ({c.name}, M={M}, ctx={ctx}, {args.gemm_target} GEMMs)",
             "bytes_per_launch": int(byts), "ms_per_launch": round(t * 1e3, 4), "peak_source": src,
             "gemm_kernel": gemm_roofline(target, M, peak) if args.gemm_target == "tcgen05" else None,
@@ -831,8 +838,10 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    # 20 prompts (the driver's sample): PEARL's per-decode spread is wide (5 prompts
+    # gave 1388-1681 tok/s for one code / calibration pair; 20 give 1311-1332)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pair", default="llama2-7b/68m")
     ap.add_argument("--gamma", type=int, default=4, help="initial draft length of adaptive PEARL")
