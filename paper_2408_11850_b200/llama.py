@@ -111,7 +111,9 @@ PAIR_BRANCH_STD = {"llama2-7b/68m": 5e-4, "dsc-33b/1.3b": 1.7e-4, "llama3-70b/8b
 # sweep with the round-2 kernels (tools/gpu_draftsms.sh, T=1, live planner
 # calibration): PEARL 1158 / 1372 / 1378 / 1451 / 1341 tok/s at 16 / 24 / 32 /
 # 40 / 48 SMs; session 3, with the single-token GEMV (tools/_r2s3_draftsms.sh):
-# 1529 / 1761 / 1455 / 1473 tok/s at 24 / 32 / 40 / 48 SMs.  DSC-33B/1.3B (prompt 512): 48 SMs (round 1: shared 130 tok/s, 48
+# 1529 / 1761 / 1455 / 1473 tok/s at 24 / 32 / 40 / 48 SMs on 5 prompts, which is
+# noise: on 20 prompts 1332 / 1337 / 1334 / 1260 (profiles/r02_s3/draftsms20_*.json).
+# DSC-33B/1.3B (prompt 512): 48 SMs (round 1: shared 130 tok/s, 48
 # SMs 163).  Llama-3 (V = 128256) needs 16-CTA clusters for its pick / verify,
 # which a partition cannot host: shared SMs.
 PAIR_DRAFT_SMS = {"llama2-7b/68m": 32, "dsc-33b/1.3b": 48, "llama3-70b/8b": 0, "tiny": 0}
