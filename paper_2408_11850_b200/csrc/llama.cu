@@ -540,6 +540,54 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv1n_kernel(const bf16* 
   if (active && lane == 0) epilogue4(e, 0, n0, acc, N);
 }
 
+// Single-token GEMV with a bf16 operand (no fused norm: the 68M o / down
+// projections), one row per warp, all of a lane's CB weight AND operand chunks
+// requested before any is used -- no smem staging, no block barrier before
+// the FMAs.  Bitwise gemv_block's rows.
+template <int CB>
+__global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv1x_kernel(const bf16* __restrict__ W,
+                                                                   const bf16* __restrict__ X, int N, int K, EpiArgs e) {
+  __shared__ float s_out[kGemvWarps];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = blockIdx.x * kGemvWarps + warp;
+  const bool active = n0 < N;
+  uint4 wr[CB], xr[CB];
+#pragma unroll
+  for (int u = 0; u < CB; ++u) {
+    const int k = u * 256 + lane * 8;
+    wr[u] = (active && k < K) ? ld_nc_v4(W + static_cast<size_t>(n0) * K + k) : make_uint4(0, 0, 0, 0);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (e.adv_pos != nullptr && blockIdx.x == 0 && tid == 0) *e.adv_pos += e.adv_n;
+#pragma unroll
+  for (int u = 0; u < CB; ++u) {
+    const int k = u * 256 + lane * 8;
+    xr[u] = k < K ? __ldg(reinterpret_cast<const uint4*>(X + k)) : make_uint4(0, 0, 0, 0);
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int u = 0; u < CB; ++u) {
+    const int k = u * 256 + lane * 8;
+    if (active && k < K) {
+      float xv[8], w[8];
+      bf16x8_to_f32(xr[u], xv);
+      bf16x8_to_f32(wr[u], w);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc = fmaf(w[j], xv[j], acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) s_out[warp] = acc;
+  __syncthreads();
+  const int nq = blockIdx.x * kGemvWarps + 4 * tid;
+  if (tid < kGemvWarps / 4 && nq < N) {
+    float v[4] = {s_out[4 * tid], s_out[4 * tid + 1], s_out[4 * tid + 2], s_out[4 * tid + 3]};
+    epilogue4(e, 0, nq, v, N);
+  }
+}
+
 // residency: at least 6 blocks per SM for the short single-batch rows (the
 // 68M draft's qkv / gate_up grids in one wave), 3 for 4-row warps, 2 for CB = 12
 // and the embedding-fold variants (one launch per token: no spills)
@@ -666,6 +714,16 @@ static bool gemv1n_enabled() {
   return on;
 }
 
+// PEARL_GEMV1X=0: bf16-operand single-token GEMVs stage the operand in smem
+// (gemv1_kernel) instead of holding it in registers (gemv1x_kernel; A/B)
+static bool gemv1x_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PEARL_GEMV1X");
+    return !(v && std::atoi(v) == 0);
+  }();
+  return on;
+}
+
 template <int NV>
 int launch_gemv1n(const bf16* W, int N, const EpiArgs& e, cudaStream_t st, const GemvNorm& nrm) {
   const dim3 grid((N + kGemvWarps * 4 - 1) / (kGemvWarps * 4)), block(kGemvWarps * 32);
@@ -690,6 +748,10 @@ int launch_gemv(const bf16* W, const bf16* X, int M, int N, int K, const EpiArgs
   const int nchunk = (K + 255) / 256;
   if (narrow) {
     const dim3 grid((N + kGemvWarps - 1) / kGemvWarps);
+    if (m1 && nrm.xh == nullptr && nrm.emb == nullptr && gemv1x_enabled()) {
+      if (nchunk <= 4) return launch_pdl(gemv1x_kernel<4>, grid, block, 0, st, W, X, N, K, e);
+      if (nchunk <= 12) return launch_pdl(gemv1x_kernel<12>, grid, block, 0, st, W, X, N, K, e);
+    }
     if (m1 && nrm.emb != nullptr && nchunk <= 4)
       return launch_pdl(gemv1_kernel<1, 4, true>, grid, block, 0, st, W, X, N, K, e, nrm);
     if (m1 && nrm.emb != nullptr) return launch_pdl(gemv1_kernel<1, 12, true>, grid, block, 0, st, W, X, N, K, e, nrm);
